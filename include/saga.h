@@ -1,0 +1,192 @@
+/*
+ * saga.h -- C ABI of the B200-native SAGA-NN layer library (libsaga.so).
+ *
+ * One GNN layer at inference in the SAGA-NN decomposition of Zhang et al.,
+ * "Architectural Implications of Graph Neural Networks" (IEEE CAL 2020,
+ * arXiv 2009.00804): Scatter -> ApplyEdge -> Gather -> ApplyVertex
+ * (Section 2; Table 1 `tbl:benchmark`, lines
+ * 176-180).  The operations and their exact definitions are the ones the
+ * fp64 oracle (oracle/oracle.c) writes out; DESIGN.md lists every reading of
+ * the paper they rest on (A1..A23).
+ *
+ * Conventions shared by every entry point
+ *  - All array arguments are DEVICE pointers (CUDA global memory on the
+ *    current device) unless marked "host".  Matrices are row-major and
+ *    contiguous; every feature/weight/output/workspace pointer must be
+ *    16-byte aligned (SAGA_EINVAL otherwise).
+ *  - Work is enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and is asynchronous: buffers must stay alive until the stream
+ *    reaches that point.  The caller owns every buffer it passes; the library
+ *    never frees them.  The only host<->device synchronisation in the library
+ *    is the range check inside saga_graph_build.
+ *  - Every function returns a saga_status; no C++ exception crosses the ABI.
+ *    On failure, saga_last_error() returns a thread-local message valid until
+ *    the next call on the same thread.  Nothing is enqueued when a call fails
+ *    its argument checks.
+ */
+#ifndef SAGA_H_
+#define SAGA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAGA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SAGA_API __attribute__((visibility("default")))
+#else
+#define SAGA_API
+#endif
+
+typedef enum {
+    SAGA_OK = 0,
+    SAGA_EINVAL = 1,       /* bad pointer / alignment / size / workspace too small   */
+    SAGA_ERANGE = 2,       /* a COO entry is out of range (see saga_graph_build)      */
+    SAGA_ESHAPE = 3,       /* tensor shape does not match graph or options            */
+    SAGA_EDTYPE = 4,       /* dtype combination not allowed for the model             */
+    SAGA_ENOMEM = 5,       /* device allocation failed                                */
+    SAGA_ECUDA = 6,        /* CUDA runtime / launch error (message has details)       */
+    SAGA_EUNSUPPORTED = 7, /* valid request this build does not implement             */
+    SAGA_EINTERNAL = 8
+} saga_status;
+
+typedef enum { SAGA_F32 = 0, SAGA_BF16 = 1 } saga_dtype;
+
+/* Table 1 rows this library implements. */
+typedef enum {
+    SAGA_GCN = 0,   /* Gather sum(in_edges) with D^-1/2 (A+I) D^-1/2 weights, ApplyVertex MLP  */
+    SAGA_SAGE = 1,  /* Gather mean(in_edges) + vertex, ApplyVertex MLP on [x || mean]          */
+    SAGA_GAT = 2,   /* ApplyEdge attention score, Gather attention(in_edges), ELU              */
+    SAGA_GATED = 3  /* per-edge-type message W_t, Gather sum(in_edges), ApplyVertex GRU        */
+} saga_model;
+
+typedef enum { SAGA_ACT_NONE = 0, SAGA_ACT_RELU = 1, SAGA_ACT_ELU = 2 } saga_act;
+
+/* Opaque, immutable after saga_graph_build; safe to share between streams. */
+typedef struct saga_graph saga_graph;
+
+/* A dense row-major device matrix [rows][cols]. */
+typedef struct {
+    void *data;
+    int32_t dtype;  /* saga_dtype */
+    int64_t rows, cols;
+} saga_tensor;
+
+typedef struct {
+    int32_t in_dim, out_dim;  /* feature widths (GAT: out_dim = heads * head_dim)         */
+    int32_t heads, head_dim;  /* GAT only (else ignored)                                  */
+    int32_t act;              /* saga_act applied by ApplyVertex: GCN/SAGE (RELU or NONE); */
+                              /* GAT must be ELU; GATED ignores it (GRU)                   */
+    float leaky_slope;        /* GAT LeakyReLU negative slope (0.2 in config C3)          */
+} saga_layer_opts;
+
+/* Weights (device, row-major, [in][out] orientation = x . W, reading A8).
+ * Unused members may be NULL.                                               */
+typedef struct {
+    const void *W;         /* GCN [in][out]; SAGE [2*in][out] (self rows first); GAT [in][heads*hd];
+                              dtype = features dtype                                              */
+    const float *bias;     /* [out] fp32, nullable (= 0)                                           */
+    const float *attn_src; /* GAT [heads][hd] fp32 (applied to the source z)                      */
+    const float *attn_dst; /* GAT [heads][hd] fp32 (applied to the destination z)                 */
+    const float *W_type;   /* GATED [T][f][f] fp32                                                 */
+    const float *W_ih;     /* GATED [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form)      */
+    const float *W_hh;     /* GATED [3][f][f] fp32                                                 */
+    const float *b_ih;     /* GATED [3][f] fp32                                                    */
+    const float *b_hh;     /* GATED [3][f] fp32                                                    */
+} saga_weights;
+
+/* Returns SAGA_ABI_VERSION. */
+SAGA_API int saga_abi_version(void);
+
+/*
+ * saga_graph_build -- COO edge list -> destination-sorted CSR (S0).
+ *
+ * Definition: PAPER.md line 130 (a layer's input is the graph "in the form
+ * of adjacency matrix") and lines 351-354 (adjacency row = destination
+ * vertex, nonzero = one of its in-edges).  Reading A7: row v holds v's
+ * in-edges in ascending COO index (a stable sort by dst); multiplicity and
+ * self-loops are kept exactly as given (no implicit self-loops, A2).
+ *
+ *  num_vertices  N >= 0;  num_edges E >= 0 (E < 2^31)
+ *  src, dst      int32[E] device, COO edge u -> v = (src[i], dst[i])
+ *  etype         int32[E] device or NULL (then all types are 0 and T = 1);
+ *                must lie in [0, num_etypes)
+ *  cuda_stream   stream all device work is ordered on
+ *  out           host: receives the new graph handle (NULL on failure)
+ *  first_bad_edge host, nullable: on SAGA_ERANGE receives the LOWEST COO
+ *                index whose src, dst or etype is out of range; -1 otherwise
+ *
+ * The handle owns device arrays (row_ptr int64[N+1], col_src/edge_id/etype
+ * int32[E], in/out degree int32[N], per-vertex norms, the load-balance
+ * schedule), allocated stream-ordered; release it with saga_free.  This call
+ * synchronises `cuda_stream` once (to read the range-check result).
+ */
+SAGA_API saga_status saga_graph_build(int32_t num_vertices, int64_t num_edges, const int32_t *src,
+                             const int32_t *dst, const int32_t *etype, int32_t num_etypes,
+                             void *cuda_stream, saga_graph **out, int64_t *first_bad_edge);
+
+/* Sizes of a built graph (host outputs, each nullable). */
+SAGA_API saga_status saga_graph_info(const saga_graph *g, int32_t *num_vertices, int64_t *num_edges,
+                            int32_t *num_etypes);
+
+/*
+ * Copy the CSR arrays into caller-provided DEVICE buffers (each nullable):
+ * row_ptr int64[N+1], col_src int32[E] (= src[edge_id[p]]), edge_id int32[E]
+ * (CSR position -> COO index), etype int32[E] (in CSR order), in_deg int32[N],
+ * out_deg int32[N].  Asynchronous on cuda_stream.
+ */
+SAGA_API saga_status saga_graph_copy_csr(const saga_graph *g, int64_t *row_ptr, int32_t *col_src,
+                                int32_t *edge_id, int32_t *etype, int32_t *in_deg,
+                                int32_t *out_deg, void *cuda_stream);
+
+/* Workspace bytes saga_layer needs for (kind, g, opts); host output. */
+SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g,
+                                       const saga_layer_opts *opts, size_t *bytes);
+
+/*
+ * saga_layer -- one SAGA-NN layer (Scatter, ApplyEdge, Gather, ApplyVertex).
+ *
+ * Definitions (in SAGA order; the GPU may reorder by linearity, fold the
+ * normalisation and split reductions, which changes only rounding):
+ *  GCN   (Table 1; BASELINE.json C1/C5; A1, A2, A12):
+ *        out[v] = act( sum_{u->v} deg(u)^-1/2 deg(v)^-1/2 x[u] . W + bias )
+ *        features F32 (fused aggregate + SIMT GEMV, in_dim % 4 == 0, <= 128,
+ *        out_dim <= 64) or BF16 (tcgen05 GEMM first, then aggregation;
+ *        in_dim in {64,128,192,256}, out_dim in {64,128,256}).
+ *  SAGE  (Table 1; BASELINE.json C2; A11, A12):
+ *        out[v] = act( [x[v] || mean_{u->v} x[u]] . W + bias ), W [2*in][out]
+ *        BF16, in_dim in {64, 128}, out_dim in {64, 128, 256}.
+ *  GAT   (Table 1; BASELINE.json C3; A13, A14):
+ *        z = x . W; s(u->v,h) = LeakyReLU(z[u,h].a_src[h] + z[v,h].a_dst[h]);
+ *        out[v,h] = ELU( sum softmax_{in-edges of v}(s) z[u,h] )
+ *        BF16, in_dim in {64..256 step 64}, heads * head_dim = out_dim = 64,
+ *        head_dim = 8.
+ *  GATED (lines 142-147, Table 1; BASELINE.json C4; A6, A15, A16):
+ *        m[v] = sum_{u->v} x[u] . W_type[t(u->v)]; out[v] = GRUCell(m[v], x[v])
+ *        F32, in_dim = out_dim = 128, num_etypes <= 4.
+ *  features  [N][in_dim];  out  [N][out_dim] with the features' dtype
+ *  workspace device scratch of at least saga_layer_workspace_bytes() bytes;
+ *            contents on entry are ignored; it must not be shared by calls in
+ *            flight on other streams.
+ * Never allocates, never synchronises.  Deterministic: identical inputs give
+ * bit-identical outputs (no floating-point atomics).
+ */
+SAGA_API saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *features,
+                       const saga_weights *w, saga_tensor *out, const saga_layer_opts *opts,
+                       void *workspace, size_t workspace_bytes, void *cuda_stream);
+
+/* Release a graph (stream-ordered on the stream it was built on). NULL-safe. */
+SAGA_API void saga_free(saga_graph *g);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+SAGA_API const char *saga_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SAGA_H_ */

@@ -1,0 +1,383 @@
+// graph_build.cu -- S0 (COO -> destination-sorted CSR), S1 (per-vertex norms)
+// and S6 (merge-path load-balance schedule) on the GPU.
+//
+// Definition followed: PAPER.md line 130 (the layer input is the graph as an
+// adjacency matrix) and lines 351-354 (row = destination vertex, nonzero =
+// in-edge); reading A7: rows ordered by destination, ties in
+// ascending COO index.  Stability comes from an LSD radix sort on dst whose
+// payload starts as the COO index (each pass is a stable scatter), so the
+// result is bit-exact and independent of scheduling -- no atomics decide any
+// position.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace saga {
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 16;
+constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 keys per block
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+
+// ------------------------------------------------------------ range check ----
+__global__ void k_range_check(int32_t n, int64_t e, const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                              const int32_t *__restrict__ etype, int32_t T, unsigned long long *first_bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t s = src[i], d = dst[i];
+        bool bad = s < 0 || s >= n || d < 0 || d >= n;
+        if (etype) {
+            int32_t t = etype[i];
+            bad |= t < 0 || t >= T;
+        }
+        if (bad) atomicMin(first_bad, (unsigned long long)i);
+    }
+}
+
+__global__ void k_degrees(int64_t e, const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                          int32_t *in_deg, int32_t *out_deg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+        atomicAdd(in_deg + dst[i], 1);   // integer atomics: order-independent result
+        atomicAdd(out_deg + src[i], 1);
+    }
+}
+
+// ------------------------------------------------------------------- scan ----
+// Exclusive scan of `count` non-negative integers into int64 out[0..count]
+// (out[count] = total).  Three phases: tile sums -> scan of sums -> tiles.
+template <typename Tin>
+__device__ __forceinline__ int64_t block_scan_excl(int64_t v, int64_t *warp_sums, int64_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_sums[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    int64_t before = warp ? warp_sums[warp - 1] : 0;
+    if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+    int64_t r = before + x - v;
+    __syncthreads();
+    return r;
+}
+
+template <typename Tin>
+__global__ void k_scan_tile_sums(const Tin *__restrict__ in, int64_t count, int64_t *sums) {
+    __shared__ int64_t ws[32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+        if (base + i < count) s += (int64_t)in[base + i];
+    int64_t tot;
+    block_scan_excl<Tin>(s, ws, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+template <typename Tin>
+__global__ void k_scan_tiles(const Tin *__restrict__ in, int64_t count, const int64_t *__restrict__ tile_offs,
+                             int64_t *out) {
+    __shared__ int64_t ws[32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int64_t v[kScanItems];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = base + i < count ? (int64_t)in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t tot;
+    int64_t run = block_scan_excl<Tin>(s, ws, &tot) + tile_offs[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < count) out[base + i] = run;
+        run += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[count] = run;
+}
+
+template <typename Tin>
+cudaError_t scan_exclusive(const Tin *in, int64_t count, int64_t *out, cudaStream_t st) {
+    if (count == 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+    int64_t tiles = (count + kScanTile - 1) / kScanTile;
+    if (tiles == 1) {
+        int64_t *zero;
+        cudaError_t err = cudaMallocAsync(&zero, sizeof(int64_t), st);
+        if (err) return err;
+        cudaMemsetAsync(zero, 0, sizeof(int64_t), st);
+        k_scan_tiles<Tin><<<1, kScanThreads, 0, st>>>(in, count, zero, out);
+        cudaFreeAsync(zero, st);
+        return cudaGetLastError();
+    }
+    int64_t *sums = nullptr, *offs = nullptr;
+    cudaError_t err = cudaMallocAsync(&sums, sizeof(int64_t) * tiles, st);
+    if (err) return err;
+    err = cudaMallocAsync(&offs, sizeof(int64_t) * (tiles + 1), st);
+    if (err) return err;
+    k_scan_tile_sums<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, sums);
+    err = scan_exclusive<int64_t>(sums, tiles, offs, st);
+    if (err) return err;
+    k_scan_tiles<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, offs, out);
+    cudaFreeAsync(sums, st);
+    cudaFreeAsync(offs, st);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- radix sort ----
+// One LSD pass over digit (key >> shift) & 255.  Histogram layout is
+// digit-major: hist[d * nblocks + b], so its exclusive scan gives every
+// (digit, block) its global output offset; within a block, keys keep their
+// input order (rank = #earlier equal digits), so the pass is stable.
+__global__ void k_radix_hist(const int32_t *__restrict__ keys, int64_t e, int shift, int32_t *hist,
+                             int64_t nblocks) {
+    __shared__ int32_t h[kRadix];
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; ++r) {
+        int64_t i = base + r * kSortThreads + threadIdx.x;
+        if (i < e) atomicAdd(&h[(keys[i] >> shift) & (kRadix - 1)], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) hist[(int64_t)i * nblocks + blockIdx.x] = h[i];
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const int32_t *__restrict__ keys_in,
+                                                                const int32_t *__restrict__ vals_in, int64_t e,
+                                                                int shift, const int64_t *__restrict__ offs,
+                                                                int64_t nblocks, int32_t *keys_out,
+                                                                int32_t *vals_out) {
+    constexpr int kWarps = kSortThreads / 32;
+    __shared__ int32_t wcnt[kWarps][kRadix];
+    __shared__ int64_t gofs[kRadix];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int d = tid; d < kRadix; d += kSortThreads) gofs[d] = offs[(int64_t)d * nblocks + blockIdx.x];
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; ++r) {
+        for (int w = 0; w < kWarps; ++w) wcnt[w][tid] = 0;  // kSortThreads == kRadix
+        __syncthreads();
+        int64_t i = base + r * kSortThreads + tid;
+        bool valid = i < e;
+        int32_t key = valid ? keys_in[i] : 0;
+        int32_t val = valid ? (vals_in ? vals_in[i] : (int32_t)i) : 0;
+        int digit = (key >> shift) & (kRadix - 1);
+        uint32_t peers = __match_any_sync(0xffffffffu, valid ? digit : (kRadix + lane));
+        int rank = __popc(peers & lt_mask);
+        if (valid && rank == 0) wcnt[warp][digit] = __popc(peers);
+        __syncthreads();
+        {   // per digit: exclusive prefix over warps (warp order == input order)
+            int64_t run = 0;
+            int32_t cnts[kWarps];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) cnts[w] = wcnt[w][tid];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                wcnt[w][tid] = (int32_t)run;
+                run += cnts[w];
+            }
+            __syncthreads();
+            if (valid) {
+                int64_t pos = gofs[digit] + wcnt[warp][digit] + rank;
+                keys_out[pos] = key;
+                vals_out[pos] = val;
+            }
+            __syncthreads();
+            gofs[tid] += run;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_iota(int32_t *p, int64_t e) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+
+__global__ void k_gather_csr(int64_t e, const int32_t *__restrict__ edge_id, const int32_t *__restrict__ src,
+                             const int32_t *__restrict__ etype, int32_t *col_src, int32_t *etype_csr) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < e; p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t id = edge_id[p];
+        col_src[p] = src[id];
+        if (etype) etype_csr[p] = etype[id];
+    }
+}
+
+// S1: dinv = deg^-1/2 (GCN, reading A1), inv_deg = 1/deg (SAGE mean); 0 for deg 0 (A12).
+__global__ void k_norms(int32_t n, const int32_t *__restrict__ in_deg, float *dinv, float *inv_deg) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int32_t d = in_deg[v];
+        float fd = (float)d;
+        dinv[v] = d > 0 ? 1.0f / sqrtf(fd) : 0.0f;
+        inv_deg[v] = d > 0 ? 1.0f / fd : 0.0f;
+    }
+}
+
+// S6: merge-path coordinates.  Items: row v's edges are items
+// row_ptr[v] + v .. row_ptr[v+1] + v - 1, its end marker is item
+// row_ptr[v+1] + v.  Task k starts at diagonal d = min(kT, E+N) at row
+// v = #rows whose end item is < d, edge position p = d - v.
+__global__ void k_merge_path(int32_t n, int64_t e, const int64_t *__restrict__ row_ptr, int64_t T, int64_t ntasks,
+                             int32_t *task_v, int64_t *task_p) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k > ntasks) return;
+    int64_t d = min(k * T, e + (int64_t)n);
+    int32_t lo = 0, hi = n;  // smallest v in [0, n] with v == n or row_ptr[v+1] + v >= d
+    while (lo < hi) {
+        int32_t mid = lo + ((hi - lo) >> 1);
+        if (row_ptr[mid + 1] + mid >= d)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    task_v[k] = lo;
+    task_p[k] = d - lo;
+}
+
+unsigned grid_for(int64_t work, int threads) {
+    int64_t b = (work + threads - 1) / threads;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)kNumSMs * 32));
+}
+
+}  // namespace
+
+#define SAGA_TRY(x)                                   \
+    do {                                              \
+        cudaError_t _e = (x);                         \
+        if (_e != cudaSuccess) {                      \
+            *why = cudaGetErrorString(_e);            \
+            return _e == cudaErrorMemoryAllocation ? SAGA_ENOMEM : SAGA_ECUDA; \
+        }                                             \
+    } while (0)
+
+saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t *dst, const int32_t *etype,
+                        int32_t num_etypes, cudaStream_t st, GraphDev *g, int64_t *first_bad, const char **why) {
+    g->n = n;
+    g->e = e;
+    g->num_etypes = etype ? num_etypes : 1;
+    g->stream = st;
+    *first_bad = -1;
+
+    // 1. range check (the library's only host sync)
+    if (e > 0) {
+        unsigned long long *bad_d;
+        SAGA_TRY(cudaMallocAsync(&bad_d, sizeof(unsigned long long), st));
+        SAGA_TRY(cudaMemsetAsync(bad_d, 0xFF, sizeof(unsigned long long), st));
+        k_range_check<<<grid_for(e, 256), 256, 0, st>>>(n, e, src, dst, etype, num_etypes, bad_d);
+        SAGA_TRY(cudaGetLastError());
+        unsigned long long bad_h = 0;
+        SAGA_TRY(cudaMemcpyAsync(&bad_h, bad_d, sizeof bad_h, cudaMemcpyDeviceToHost, st));
+        SAGA_TRY(cudaStreamSynchronize(st));
+        cudaFreeAsync(bad_d, st);
+        if (bad_h != ~0ull) {
+            *first_bad = (int64_t)bad_h;
+            *why = "COO entry out of range";
+            return SAGA_ERANGE;
+        }
+    }
+
+    const size_t nn = (size_t)std::max(n, 1), ne = (size_t)std::max<int64_t>(e, 1);
+    SAGA_TRY(cudaMallocAsync(&g->row_ptr, sizeof(int64_t) * (nn + 1), st));
+    SAGA_TRY(cudaMallocAsync(&g->col_src, sizeof(int32_t) * ne, st));
+    SAGA_TRY(cudaMallocAsync(&g->edge_id, sizeof(int32_t) * ne, st));
+    if (etype) SAGA_TRY(cudaMallocAsync(&g->etype, sizeof(int32_t) * ne, st));
+    SAGA_TRY(cudaMallocAsync(&g->in_deg, sizeof(int32_t) * nn, st));
+    SAGA_TRY(cudaMallocAsync(&g->out_deg, sizeof(int32_t) * nn, st));
+    SAGA_TRY(cudaMallocAsync(&g->dinv, sizeof(float) * nn, st));
+    SAGA_TRY(cudaMallocAsync(&g->inv_deg, sizeof(float) * nn, st));
+    SAGA_TRY(cudaMemsetAsync(g->in_deg, 0, sizeof(int32_t) * nn, st));
+    SAGA_TRY(cudaMemsetAsync(g->out_deg, 0, sizeof(int32_t) * nn, st));
+
+    // 2. degrees, 3. row_ptr
+    if (e > 0) k_degrees<<<grid_for(e, 256), 256, 0, st>>>(e, src, dst, g->in_deg, g->out_deg);
+    SAGA_TRY(cudaGetLastError());
+    SAGA_TRY(scan_exclusive<int32_t>(g->in_deg, n, g->row_ptr, st));
+
+    // 4. stable LSD radix sort of (dst, COO index)
+    if (e > 0) {
+        int bits = 0;
+        while (bits < 31 && (int64_t(1) << bits) < (int64_t)n) ++bits;   // keys < n <= 2^bits
+        int passes = (bits + kRadixBits - 1) / kRadixBits;
+        if (passes == 0) {
+            k_iota<<<grid_for(e, 256), 256, 0, st>>>(g->edge_id, e);
+        } else {
+            int64_t nblocks = (e + kSortTile - 1) / kSortTile;
+            int32_t *kbuf[2], *vbuf[2], *hist;
+            int64_t *offs;
+            SAGA_TRY(cudaMallocAsync(&kbuf[0], sizeof(int32_t) * e, st));
+            SAGA_TRY(cudaMallocAsync(&kbuf[1], sizeof(int32_t) * e, st));
+            SAGA_TRY(cudaMallocAsync(&vbuf[0], sizeof(int32_t) * e, st));
+            SAGA_TRY(cudaMallocAsync(&vbuf[1], sizeof(int32_t) * e, st));
+            SAGA_TRY(cudaMallocAsync(&hist, sizeof(int32_t) * kRadix * nblocks, st));
+            SAGA_TRY(cudaMallocAsync(&offs, sizeof(int64_t) * (kRadix * nblocks + 1), st));
+            const int32_t *kin = dst;
+            const int32_t *vin = nullptr;  // pass 0 payload = COO index
+            for (int pass = 0; pass < passes; ++pass) {
+                int shift = pass * kRadixBits;
+                int32_t *kout = kbuf[pass & 1], *vout = (pass == passes - 1) ? g->edge_id : vbuf[pass & 1];
+                k_radix_hist<<<(unsigned)nblocks, kSortThreads, 0, st>>>(kin, e, shift, hist, nblocks);
+                SAGA_TRY(cudaGetLastError());
+                SAGA_TRY(scan_exclusive<int32_t>(hist, kRadix * nblocks, offs, st));
+                k_radix_scatter<<<(unsigned)nblocks, kSortThreads, 0, st>>>(kin, vin, e, shift, offs, nblocks, kout,
+                                                                            vout);
+                SAGA_TRY(cudaGetLastError());
+                kin = kout;
+                vin = vout;
+            }
+            cudaFreeAsync(kbuf[0], st);
+            cudaFreeAsync(kbuf[1], st);
+            cudaFreeAsync(vbuf[0], st);
+            cudaFreeAsync(vbuf[1], st);
+            cudaFreeAsync(hist, st);
+            cudaFreeAsync(offs, st);
+        }
+        k_gather_csr<<<grid_for(e, 256), 256, 0, st>>>(e, g->edge_id, src, etype, g->col_src, g->etype);
+        SAGA_TRY(cudaGetLastError());
+    }
+    if (n > 0) k_norms<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, g->dinv, g->inv_deg);
+    SAGA_TRY(cudaGetLastError());
+
+    // 6. merge-path schedule: ~ 4 tasks per resident warp of a 148-SM part
+    int64_t items = e + (int64_t)n;
+    int64_t target = (int64_t)kNumSMs * 64 * 4;
+    int64_t T = std::max<int64_t>(32, (items + target - 1) / target);
+    g->task_items = T;
+    g->ntasks = items > 0 ? (items + T - 1) / T : 0;
+    SAGA_TRY(cudaMallocAsync(&g->task_v, sizeof(int32_t) * (g->ntasks + 1), st));
+    SAGA_TRY(cudaMallocAsync(&g->task_p, sizeof(int64_t) * (g->ntasks + 1), st));
+    if (n > 0)
+        k_merge_path<<<(unsigned)((g->ntasks + 1 + 255) / 256), 256, 0, st>>>(n, e, g->row_ptr, T, g->ntasks,
+                                                                              g->task_v, g->task_p);
+    SAGA_TRY(cudaGetLastError());
+    return SAGA_OK;
+}
+
+void free_graph(GraphDev *g) {
+    cudaStream_t st = g->stream;
+    void *ptrs[] = {g->row_ptr, g->col_src, g->edge_id, g->etype, g->in_deg, g->out_deg,
+                    g->dinv,    g->inv_deg, g->task_v,  g->task_p};
+    for (void *p : ptrs)
+        if (p) cudaFreeAsync(p, st);
+}
+
+}  // namespace saga

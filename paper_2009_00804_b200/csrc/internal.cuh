@@ -1,0 +1,90 @@
+// internal.cuh -- shared declarations of the CUDA path (not part of the ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/saga.h"
+
+namespace saga {
+
+constexpr int kNumSMs = 148;
+
+// Device arrays owned by a built graph (saga_graph_build, S0).
+struct GraphDev {
+    int32_t n = 0;
+    int64_t e = 0;
+    int32_t num_etypes = 1;
+    int64_t *row_ptr = nullptr;   // [n+1]
+    int32_t *col_src = nullptr;   // [e]
+    int32_t *edge_id = nullptr;   // [e]
+    int32_t *etype = nullptr;     // [e] (nullptr when no types were given)
+    int32_t *in_deg = nullptr;    // [n]
+    int32_t *out_deg = nullptr;   // [n]
+    float *dinv = nullptr;        // [n]  in_deg^-1/2 (0 if 0)  -- S1, GCN
+    float *inv_deg = nullptr;     // [n]  1/in_deg (0 if 0)     -- S1, SAGE
+    // Merge-path load-balance schedule (S6): items = E edges + N row ends,
+    // task k covers items [k*T, min((k+1)T, E+N)); its start coordinate is
+    // (task_v[k], task_p[k]).  Arrays have ntasks+1 entries.
+    int64_t task_items = 0;       // T
+    int64_t ntasks = 0;
+    int32_t *task_v = nullptr;
+    int64_t *task_p = nullptr;
+    cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
+};
+
+// Graph build (graph_build.cu). Returns cudaError / ERANGE via first_bad.
+saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t *dst, const int32_t *etype,
+                        int32_t num_etypes, cudaStream_t st, GraphDev *g, int64_t *first_bad, const char **why);
+void free_graph(GraphDev *g);
+
+// ---------------------------------------------------------- aggregation ----
+// Merge-path segment-reduce family (aggregate.cu).  Partials/counters live in
+// the caller's workspace; counters must be zero on entry (host memsets).
+struct AggWorkspace {
+    int32_t *counters = nullptr;  // [ntasks]
+    float *partials = nullptr;    // [2*ntasks][partial_floats]
+};
+size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads);
+
+// C5 / bf16 GCN: out[v] = act(dinv[v] * sum Y[u] + bias), Y already scaled by dinv[u].
+cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
+                                __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
+// C1 / fp32 GCN fused: out[v] = act((dinv[v] * sum dinv[u] x[u]) . W + bias).
+cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
+                                 const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st);
+// SAGE: M[v] = inv_deg[v] * sum x[u]  (bf16 out)
+cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
+                                 AggWorkspace ws, cudaStream_t st);
+// GAT fused edge kernel: online softmax + aggregate + ELU.
+cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
+                            float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
+// GATED typed sums: S[v][t][:] = sum_{type t} H[u]  (fp32)
+cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, AggWorkspace ws,
+                                 cudaStream_t st);
+
+// ----------------------------------------------------------------- GEMM ----
+enum GemmEpi { EPI_ROWSCALE = 0, EPI_BIAS_ACT = 1, EPI_GAT = 2 };
+struct GemmArgs {
+    int64_t M = 0;
+    int32_t K0 = 0, K1 = 0;          // K split over two A sources (K1 = 0: one source)
+    int32_t N = 0;
+    const __nv_bfloat16 *A0 = nullptr, *A1 = nullptr;  // [M][K0], [M][K1]
+    const __nv_bfloat16 *W = nullptr;                  // [K0+K1][N] row-major
+    __nv_bfloat16 *out = nullptr;                      // [M][N]
+    GemmEpi epi = EPI_ROWSCALE;
+    const float *row_scale = nullptr;                  // EPI_ROWSCALE
+    const float *bias = nullptr;                       // EPI_BIAS_ACT
+    int act = 0;
+    const float *a_src = nullptr, *a_dst = nullptr;    // EPI_GAT [heads][8]
+    float *el = nullptr, *er = nullptr;                // EPI_GAT [M][heads]
+};
+cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char **why);
+
+// fp32 GEMM + GRU (gemm_f32.cu), config C4.
+cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, const float *H, const float *W_type,
+                               const float *W_ih, const float *W_hh, const float *b_ih, const float *b_hh,
+                               float *m_ws, float *out, cudaStream_t st);
+
+}  // namespace saga

@@ -1,0 +1,294 @@
+// saga_host.cu -- the C ABI (include/saga.h): argument validation, workspace
+// planning and kernel sequencing for one SAGA-NN layer.  No allocation and no
+// synchronisation on the layer path; every launch goes on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.cuh"
+
+struct saga_graph {
+    saga::GraphDev d;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+saga_status fail(saga_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+saga_status fail(saga_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+saga_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(e == cudaErrorMemoryAllocation ? SAGA_ENOMEM : SAGA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Workspace plan: [counters | partials | model intermediates].
+struct Plan {
+    size_t counters = 0, partials = 0, inter0 = 0, inter1 = 0, inter2 = 0, total = 0;
+};
+
+Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
+    Plan p;
+    const size_t nt = (size_t)g.ntasks;
+    const size_t n = (size_t)g.n;
+    size_t width = 0;
+    switch (kind) {
+        case SAGA_GCN: width = (size_t)(o.in_dim <= 0 ? 0 : (o.out_dim > 0 ? o.out_dim : 0)); break;
+        case SAGA_SAGE: width = (size_t)o.in_dim; break;
+        case SAGA_GAT: width = (size_t)o.out_dim; break;
+        case SAGA_GATED: width = (size_t)o.in_dim; break;
+    }
+    size_t pf = saga::agg_partial_floats(kind, (int32_t)width, 8);
+    if (kind == SAGA_GCN) pf = (size_t)std::max(o.in_dim, o.out_dim);  // covers the fp32 agg-first path too
+    p.counters = align_up(sizeof(int32_t) * (nt + 1));
+    p.partials = align_up(sizeof(float) * pf * 2 * (nt + 1));
+    switch (kind) {
+        case SAGA_GCN: p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0)); break;  // Y bf16
+        case SAGA_SAGE: p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0)); break;  // M bf16
+        case SAGA_GAT:
+            p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0));               // z bf16
+            p.inter1 = align_up(sizeof(float) * n * 8);                                         // el
+            p.inter2 = align_up(sizeof(float) * n * 8);                                         // er
+            break;
+        case SAGA_GATED:
+            p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S
+            p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
+            break;
+    }
+    p.total = p.counters + p.partials + p.inter0 + p.inter1 + p.inter2;
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int saga_abi_version(void) { return SAGA_ABI_VERSION; }
+
+const char *saga_last_error(void) { return g_last_error.c_str(); }
+
+saga_status saga_graph_build(int32_t num_vertices, int64_t num_edges, const int32_t *src, const int32_t *dst,
+                             const int32_t *etype, int32_t num_etypes, void *cuda_stream, saga_graph **out,
+                             int64_t *first_bad_edge) {
+    g_last_error.clear();
+    if (first_bad_edge) *first_bad_edge = -1;
+    if (!out) return fail(SAGA_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_vertices < 0 || num_edges < 0 || num_edges >= (int64_t(1) << 31))
+        return fail(SAGA_EINVAL, "invalid sizes N=%d E=%lld", num_vertices, (long long)num_edges);
+    if (num_edges > 0 && (!src || !dst)) return fail(SAGA_EINVAL, "src/dst is NULL");
+    if (etype && num_etypes < 1) return fail(SAGA_EINVAL, "num_etypes must be >= 1 with etype");
+    if (num_vertices == 0 && num_edges > 0) {
+        if (first_bad_edge) *first_bad_edge = 0;
+        return fail(SAGA_ERANGE, "COO entry 0 out of range (N = 0)");
+    }
+    saga_graph *g = new (std::nothrow) saga_graph();
+    if (!g) return fail(SAGA_ENOMEM, "host allocation failed");
+    int64_t bad = -1;
+    const char *why = "";
+    saga_status s = saga::build_graph(num_vertices, num_edges, src, dst, etype, num_etypes,
+                                      static_cast<cudaStream_t>(cuda_stream), &g->d, &bad, &why);
+    if (s != SAGA_OK) {
+        if (first_bad_edge) *first_bad_edge = bad;
+        saga::free_graph(&g->d);
+        delete g;
+        if (s == SAGA_ERANGE) return fail(s, "COO entry %lld out of range", (long long)bad);
+        return fail(s, "graph build failed: %s", why);
+    }
+    *out = g;
+    return SAGA_OK;
+}
+
+saga_status saga_graph_info(const saga_graph *g, int32_t *n, int64_t *e, int32_t *t) {
+    if (!g) return fail(SAGA_EINVAL, "graph is NULL");
+    if (n) *n = g->d.n;
+    if (e) *e = g->d.e;
+    if (t) *t = g->d.num_etypes;
+    return SAGA_OK;
+}
+
+saga_status saga_graph_copy_csr(const saga_graph *g, int64_t *row_ptr, int32_t *col_src, int32_t *edge_id,
+                                int32_t *etype, int32_t *in_deg, int32_t *out_deg, void *cuda_stream) {
+    if (!g) return fail(SAGA_EINVAL, "graph is NULL");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const saga::GraphDev &d = g->d;
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void *dst, const void *srcp, size_t bytes) {
+        if (dst && bytes && e == cudaSuccess) e = cudaMemcpyAsync(dst, srcp, bytes, cudaMemcpyDeviceToDevice, st);
+    };
+    cp(row_ptr, d.row_ptr, sizeof(int64_t) * ((size_t)d.n + 1));
+    cp(col_src, d.col_src, sizeof(int32_t) * (size_t)d.e);
+    cp(edge_id, d.edge_id, sizeof(int32_t) * (size_t)d.e);
+    if (etype) {
+        if (d.etype)
+            cp(etype, d.etype, sizeof(int32_t) * (size_t)d.e);
+        else if (d.e && e == cudaSuccess)
+            e = cudaMemsetAsync(etype, 0, sizeof(int32_t) * (size_t)d.e, st);
+    }
+    cp(in_deg, d.in_deg, sizeof(int32_t) * (size_t)d.n);
+    cp(out_deg, d.out_deg, sizeof(int32_t) * (size_t)d.n);
+    return e ? cuda_fail(e, "copy_csr") : SAGA_OK;
+}
+
+saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g, const saga_layer_opts *opts,
+                                       size_t *bytes) {
+    if (!g || !opts || !bytes) return fail(SAGA_EINVAL, "NULL argument");
+    if (kind < SAGA_GCN || kind > SAGA_GATED) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+    *bytes = plan_for(kind, g->d, *opts).total;
+    return SAGA_OK;
+}
+
+void saga_free(saga_graph *g) {
+    if (!g) return;
+    saga::free_graph(&g->d);
+    delete g;
+}
+
+saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *x, const saga_weights *w,
+                       saga_tensor *out, const saga_layer_opts *opts, void *workspace, size_t workspace_bytes,
+                       void *cuda_stream) {
+    using namespace saga;
+    g_last_error.clear();
+    if (!g || !x || !w || !out || !opts) return fail(SAGA_EINVAL, "NULL argument");
+    const GraphDev &d = g->d;
+    const saga_layer_opts &o = *opts;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (x->rows != d.n) return fail(SAGA_ESHAPE, "features.rows=%lld != N=%d", (long long)x->rows, d.n);
+    if (x->cols != o.in_dim) return fail(SAGA_ESHAPE, "features.cols=%lld != in_dim=%d", (long long)x->cols, o.in_dim);
+    if (out->rows != d.n || out->cols != o.out_dim)
+        return fail(SAGA_ESHAPE, "out shape [%lld][%lld] != [%d][%d]", (long long)out->rows, (long long)out->cols, d.n,
+                    o.out_dim);
+    if (out->dtype != x->dtype) return fail(SAGA_EDTYPE, "out dtype must equal features dtype");
+    if (d.n > 0 && (!x->data || !out->data)) return fail(SAGA_EINVAL, "features/out data is NULL");
+    if (!aligned16(x->data) || !aligned16(out->data) || !aligned16(workspace))
+        return fail(SAGA_EINVAL, "features/out/workspace must be 16-byte aligned");
+    const Plan plan = plan_for(kind, d, o);
+    if (workspace_bytes < plan.total || (plan.total && !workspace))
+        return fail(SAGA_EINVAL, "workspace too small: %zu < %zu", workspace_bytes, plan.total);
+    if (d.n == 0) return SAGA_OK;
+
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    AggWorkspace aw;
+    aw.counters = reinterpret_cast<int32_t *>(ws);
+    aw.partials = reinterpret_cast<float *>(ws + plan.counters);
+    uint8_t *i0 = ws + plan.counters + plan.partials;
+    uint8_t *i1 = i0 + plan.inter0;
+    uint8_t *i2 = i1 + plan.inter1;
+    cudaError_t e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)d.ntasks + 1), st);
+    if (e) return cuda_fail(e, "memset counters");
+    const char *why = "";
+
+    switch (kind) {
+        case SAGA_GCN: {
+            if (!w->W) return fail(SAGA_EINVAL, "GCN needs W");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GCN act must be NONE/RELU");
+            if (x->dtype == SAGA_F32) {
+                if (!(o.in_dim == 16 || o.in_dim == 32 || o.in_dim == 64 || o.in_dim == 128) || o.out_dim < 1 ||
+                    o.out_dim > 64)
+                    return fail(SAGA_EUNSUPPORTED, "fp32 GCN supports in_dim in {16,32,64,128}, out_dim <= 64");
+                e = launch_gcn_f32_fused(d, static_cast<const float *>(x->data), o.in_dim,
+                                         static_cast<const float *>(w->W), o.out_dim, w->bias, o.act,
+                                         static_cast<float *>(out->data), aw, st);
+                if (e) return cuda_fail(e, "gcn_f32_fused");
+                return SAGA_OK;
+            }
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GCN features must be F32 or BF16");
+            if (o.in_dim % 64 || o.in_dim > 256 || o.in_dim == 0 ||
+                !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "bf16 GCN supports in_dim in {64..256 step 64}, out_dim in {64,128,256}");
+            // S2: Y = diag(dinv) . X . W  (tcgen05), then S3-S5 aggregation
+            __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(i0);
+            GemmArgs a;
+            a.M = d.n; a.K0 = o.in_dim; a.K1 = 0; a.N = o.out_dim;
+            a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
+            a.W = static_cast<const __nv_bfloat16 *>(w->W);
+            a.out = Y;
+            a.epi = EPI_ROWSCALE;
+            a.row_scale = d.dinv;
+            e = launch_gemm_bf16_tc(a, st, &why);
+            if (e) return fail(SAGA_ECUDA, "gcn gemm: %s (%s)", cudaGetErrorString(e), why);
+            e = launch_agg_gcn_bf16(d, Y, o.out_dim, w->bias, o.act, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            if (e) return cuda_fail(e, "gcn aggregate");
+            return SAGA_OK;
+        }
+        case SAGA_SAGE: {
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE supports BF16 features");
+            if (!w->W) return fail(SAGA_EINVAL, "SAGE needs W");
+            if (!(o.in_dim == 64 || o.in_dim == 128) || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "SAGE supports in_dim in {64,128}, out_dim in {64,128,256}");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE act must be NONE/RELU");
+            __nv_bfloat16 *M = reinterpret_cast<__nv_bfloat16 *>(i0);
+            e = launch_agg_mean_bf16(d, static_cast<const __nv_bfloat16 *>(x->data), o.in_dim, M, aw, st);
+            if (e) return cuda_fail(e, "sage aggregate");
+            GemmArgs a;
+            a.M = d.n; a.K0 = o.in_dim; a.K1 = o.in_dim; a.N = o.out_dim;
+            a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
+            a.A1 = M;
+            a.W = static_cast<const __nv_bfloat16 *>(w->W);
+            a.out = static_cast<__nv_bfloat16 *>(out->data);
+            a.epi = EPI_BIAS_ACT;
+            a.bias = w->bias;
+            a.act = o.act;
+            e = launch_gemm_bf16_tc(a, st, &why);
+            if (e) return fail(SAGA_ECUDA, "sage gemm: %s (%s)", cudaGetErrorString(e), why);
+            return SAGA_OK;
+        }
+        case SAGA_GAT: {
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GAT supports BF16 features");
+            if (!w->W || !w->attn_src || !w->attn_dst) return fail(SAGA_EINVAL, "GAT needs W, attn_src, attn_dst");
+            if (o.heads != 8 || o.head_dim != 8 || o.out_dim != 64 || o.in_dim % 64 || o.in_dim > 256 || !o.in_dim)
+                return fail(SAGA_EUNSUPPORTED, "GAT supports heads=8, head_dim=8, in_dim in {64..256 step 64}");
+            if (o.act != SAGA_ACT_ELU) return fail(SAGA_EUNSUPPORTED, "GAT act must be ELU");
+            __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(i0);
+            float *el = reinterpret_cast<float *>(i1), *er = reinterpret_cast<float *>(i2);
+            GemmArgs a;
+            a.M = d.n; a.K0 = o.in_dim; a.K1 = 0; a.N = 64;
+            a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
+            a.W = static_cast<const __nv_bfloat16 *>(w->W);
+            a.out = z;
+            a.epi = EPI_GAT;
+            a.a_src = w->attn_src; a.a_dst = w->attn_dst; a.el = el; a.er = er;
+            e = launch_gemm_bf16_tc(a, st, &why);
+            if (e) return fail(SAGA_ECUDA, "gat gemm: %s (%s)", cudaGetErrorString(e), why);
+            e = launch_gat_edge(d, z, el, er, o.leaky_slope, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            if (e) return cuda_fail(e, "gat edge");
+            return SAGA_OK;
+        }
+        case SAGA_GATED: {
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GATED supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GATED supports in=out=128");
+            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "GATED supports <= 4 edge types");
+            if (!w->W_type || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "GATED needs W_type, W_ih, W_hh, b_ih, b_hh");
+            float *S = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
+            e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, aw, st);
+            if (e) return cuda_fail(e, "typed aggregate");
+            e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
+                                   w->W_ih, w->W_hh, w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
+            if (e) return cuda_fail(e, "gated apply");
+            return SAGA_OK;
+        }
+    }
+    return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+"""Test/bench glue: run a configured step on the GPU path and on the oracle.
+
+The GPU side goes only through paper_2009_00804_b200 (the C ABI); the oracle
+side only through oracle/.  Both consume the same tensors from workloads/.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import workloads as W
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}   # BASELINE.json north_star, normwise inf-relative (A18)
+
+
+def dev_inputs(d, dev):
+    return {k: (v.to(dev) if isinstance(v, torch.Tensor) else v) for k, v in d.items()}
+
+
+def gpu_graph(saga, cfg, d):
+    return saga.saga_graph_build(cfg.n, d["src"], d["dst"], d.get("etype"), cfg.num_etypes)
+
+
+def gpu_step(saga, cfg, g, d, layers=None):
+    """Run the configured step; returns list of per-layer outputs (device)."""
+    act_relu = saga.SAGA_ACT_RELU
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    if cfg.model == "gcn":
+        lay = layers[0] if layers else saga.Layer("gcn", g, cfg.dims[0], cfg.dims[1], act_relu, dt)
+        return [lay(d["X"], {"W": d["W"], "bias": d["b"]})], [lay]
+    if cfg.model == "sage":
+        f0, f1, f2 = cfg.dims
+        l1 = layers[0] if layers else saga.Layer("sage", g, f0, f1, act_relu, dt)
+        l2 = layers[1] if layers else saga.Layer("sage", g, f1, f2, saga.SAGA_ACT_NONE, dt)
+        h1 = l1(d["X"], {"W": d["W1"]})
+        return [h1, l2(h1, {"W": d["W2"]})], [l1, l2]
+    if cfg.model == "gat":
+        fi, fo = cfg.dims
+        lay = layers[0] if layers else saga.Layer("gat", g, fi, fo, saga.SAGA_ACT_ELU, dt, heads=cfg.heads,
+                                                  head_dim=fo // cfg.heads, leaky_slope=0.2)
+        return [lay(d["X"], {"W": d["W"], "attn_src": d["a_src"], "attn_dst": d["a_dst"]})], [lay]
+    if cfg.model == "gated":
+        f = cfg.dims[0]
+        lay = layers[0] if layers else saga.Layer("gated", g, f, f, saga.SAGA_ACT_NONE, dt)
+        w = {k: d[k].contiguous() for k in ("W_type", "W_ih", "W_hh", "b_ih", "b_hh")}
+        return [lay(d["H"], w)], [lay]
+    raise ValueError(cfg.model)
+
+
+def oracle_graph(oracle, cfg, d):
+    et = d.get("etype")
+    return oracle.csr_build(cfg.n, d["src"].cpu(), d["dst"].cpu(), None if et is None else et.cpu(),
+                            cfg.num_etypes)
+
+
+def oracle_step(oracle, cfg, og, d, rows=None, layer_inputs=None):
+    """fp64 reference of the configured step (list per layer).
+
+    For SAGE, layer 2 takes `layer_inputs[1]` if given (the GPU's bf16 H1,
+    per-layer parity, reading A19), else the oracle's own fp64 H1."""
+    c = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in d.items()}
+    if cfg.model == "gcn":
+        return [oracle.gcn(og, c["X"], c["W"].float(), c["b"], act=1, rows=rows)]
+    if cfg.model == "sage":
+        h1 = oracle.sage_mean(og, c["X"], c["W1"].float(), act=1, rows=None)
+        x2 = layer_inputs[1] if layer_inputs is not None else h1
+        h2 = oracle.sage_mean(og, x2, c["W2"].float(), act=0, rows=rows)
+        return [h1 if rows is None else h1[np.asarray(rows)], h2]
+    if cfg.model == "gat":
+        return [oracle.gat(og, c["X"], c["W"].float(), c["a_src"], c["a_dst"], 0.2, rows=rows)]
+    if cfg.model == "gated":
+        return [oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)]
+    raise ValueError(cfg.model)
+
+
+def to_np(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def sample_rows(og, k, seed=0):
+    """Sampled rows for full-size checks: the 16 highest in-degree rows (hubs,
+    split across tasks), first/last rows, and k uniform rows."""
+    n = og.n
+    rng = np.random.default_rng(seed)
+    hubs = np.argsort(-og.in_deg, kind="stable")[:16]
+    rows = np.concatenate([hubs, [0, n - 1], rng.integers(0, n, k)]).astype(np.int64)
+    return np.unique(rows)

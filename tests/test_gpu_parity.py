@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star): CSR and degrees bit-exact; layer outputs
+within normwise inf-relative error 1e-4 (fp32 configs) / 2e-2 (bf16 configs)
+of the fp64 oracle (reading A18).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from tests import harness as H
+from tests import zoo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def saga():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2009_00804_b200 as s
+    return s
+
+
+DEV = "cuda"
+
+
+def _csr_check(saga, n, s, d, et=None, T=1):
+    st, dt = torch.from_numpy(np.ascontiguousarray(s)), torch.from_numpy(np.ascontiguousarray(d))
+    ett = None if et is None else torch.from_numpy(np.ascontiguousarray(et))
+    g = saga.saga_graph_build(n, st.to(DEV), dt.to(DEV), None if ett is None else ett.to(DEV), T)
+    got = {k: v.cpu().numpy() for k, v in g.csr().items()}
+    og = oracle.csr_build(n, s, d, et, T)
+    np.testing.assert_array_equal(got["row_ptr"], og.row_ptr)
+    np.testing.assert_array_equal(got["col_src"], og.col_src)
+    np.testing.assert_array_equal(got["edge_id"], og.edge_id)
+    np.testing.assert_array_equal(got["etype"], og.etype)
+    np.testing.assert_array_equal(got["in_deg"], og.in_deg)
+    np.testing.assert_array_equal(got["out_deg"], og.out_deg)
+
+
+@pytest.mark.parametrize("name,n,s,d", zoo.zoo(include_big=True), ids=lambda x: x if isinstance(x, str) else "")
+def test_csr_bitexact_zoo(saga, name, n, s, d):
+    _csr_check(saga, n, s, d)
+    et = (np.arange(s.shape[0]) % 3).astype(np.int32)
+    _csr_check(saga, n, s, d, et, 3)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
+def test_csr_bitexact_configs(saga, cfg):
+    c = W.CONFIGS[cfg]
+    s, d, et = W.make_graph(c, DEV)
+    g = saga.saga_graph_build(c.n, s, d, et, c.num_etypes)
+    got = g.csr()
+    og = oracle.csr_build(c.n, s.cpu(), d.cpu(), None if et is None else et.cpu(), c.num_etypes)
+    assert torch.equal(got["row_ptr"].cpu(), torch.from_numpy(og.row_ptr))
+    assert torch.equal(got["col_src"].cpu(), torch.from_numpy(og.col_src))
+    assert torch.equal(got["edge_id"].cpu(), torch.from_numpy(og.edge_id))
+    assert torch.equal(got["in_deg"].cpu(), torch.from_numpy(og.in_deg))
+    assert torch.equal(got["out_deg"].cpu(), torch.from_numpy(og.out_deg))
+    if et is not None:
+        assert torch.equal(got["etype"].cpu(), torch.from_numpy(og.etype))
+
+
+def test_range_error_reports_lowest_index(saga):
+    s = torch.tensor([0, 1, 2, 9, 1, -1], dtype=torch.int32, device=DEV)
+    d = torch.tensor([1, 2, 0, 0, 7, 0], dtype=torch.int32, device=DEV)
+    with pytest.raises(saga.SagaError) as ei:
+        saga.saga_graph_build(3, s, d)
+    assert ei.value.status == saga.SAGA_ERANGE and ei.value.first_bad_edge == 3
+    et = torch.tensor([0, 0, 5], dtype=torch.int32, device=DEV)
+    with pytest.raises(saga.SagaError) as ei:
+        saga.saga_graph_build(3, s[:3], d[:3], et, 2)
+    assert ei.value.first_bad_edge == 2
+
+
+# ------------------------------------------------------------ layer zoo ----
+
+def _zoo_inputs(model, n, s, d, seed):
+    """Small-graph inputs for each model at supported widths."""
+    gen = torch.Generator().manual_seed(seed)
+    r = lambda *sh, sc=1.0: torch.randn(*sh, generator=gen) * sc
+    if model == "gcn_bf16":
+        return {"X": r(n, 64).bfloat16(), "W": r(64, 64, sc=0.2).bfloat16(), "b": r(64, sc=0.1)}
+    if model == "gcn_f32":
+        return {"X": r(n, 64), "W": r(64, 16, sc=0.2), "b": r(16, sc=0.1)}
+    if model == "sage":
+        return {"X": r(n, 128).bfloat16(), "W1": r(256, 128, sc=0.1).bfloat16(), "W2": r(256, 64, sc=0.1).bfloat16()}
+    if model == "gat":
+        return {"X": r(n, 256).bfloat16(), "W": r(256, 64, sc=0.1).bfloat16(), "a_src": r(8, 8, sc=0.5),
+                "a_dst": r(8, 8, sc=0.5)}
+    if model == "gated":
+        b = 1 / np.sqrt(128)
+        u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
+        return {"H": r(n, 128), "W_type": u(4, 128, 128), "W_ih": u(3, 128, 128), "W_hh": u(3, 128, 128),
+                "b_ih": u(3, 128), "b_hh": u(3, 128)}
+
+
+def _zoo_cfg(model, n, e):
+    base = {"gcn_bf16": W.Config("z", "gcn", "er", n, e, False, False, "bf16", (64, 64)),
+            "gcn_f32": W.Config("z", "gcn", "er", n, e, False, False, "f32", (64, 16)),
+            "sage": W.Config("z", "sage", "er", n, e, False, False, "bf16", (128, 128, 64)),
+            "gat": W.Config("z", "gat", "er", n, e, False, False, "bf16", (256, 64), heads=8),
+            "gated": W.Config("z", "gated", "er", n, e, False, False, "f32", (128, 128), num_etypes=4)}
+    return base[model]
+
+
+ZOO = [z for z in zoo.zoo(include_big=True) if z[1] > 0]
+MODELS = ["gcn_bf16", "gcn_f32", "sage", "gat", "gated"]
+
+
+@pytest.mark.parametrize("model", MODELS)
+@pytest.mark.parametrize("name,n,s,d", ZOO, ids=lambda x: x if isinstance(x, str) else "")
+@pytest.mark.parametrize("loops", [False, True])
+def test_layer_zoo(saga, model, name, n, s, d, loops):
+    if loops:
+        s, d = zoo.with_self_loops(n, s, d)
+    cfg = _zoo_cfg(model, n, s.shape[0])
+    x = _zoo_inputs(model, n, s, d, 7)
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    if model == "gated":
+        x["etype"] = torch.from_numpy((np.arange(s.shape[0]) * 7 % 4).astype(np.int32))
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, _ = H.gpu_step(saga, cfg, g, dx)
+    torch.cuda.synchronize()
+    og = H.oracle_graph(oracle, cfg, x)
+    refs = H.oracle_step(oracle, cfg, og, x, layer_inputs=[None, outs[0].cpu()] if model == "sage" else None)
+    tol = H.TOL[cfg.dtype]
+    for y, ref in zip(outs, refs):
+        err = oracle.rel_err(H.to_np(y), ref)
+        assert err <= tol, f"{model}/{name}: rel err {err:.3e} > {tol}"
+
+
+# ----------------------------------------------------- configured steps ----
+
+def _config_check(saga, cfg, rows_k=None):
+    d = W.make_inputs(cfg, DEV)
+    g = H.gpu_graph(saga, cfg, d)
+    outs, layers = H.gpu_step(saga, cfg, g, d)
+    outs2, _ = H.gpu_step(saga, cfg, g, d, layers)           # determinism: bitwise equal
+    torch.cuda.synchronize()
+    for a, b in zip(outs, outs2):
+        assert torch.equal(a, b)
+    og = H.oracle_graph(oracle, cfg, d)
+    rows = None if rows_k is None else H.sample_rows(og, rows_k)
+    tol = H.TOL[cfg.dtype]
+    li = [None, outs[0].cpu()] if cfg.model == "sage" else None
+    refs = H.oracle_step(oracle, cfg, og, d, rows=rows, layer_inputs=li)
+    for y, ref in zip(outs, refs):
+        yy = H.to_np(y if rows is None else y[torch.from_numpy(rows).to(y.device)])
+        err = oracle.rel_err(yy, ref)
+        assert err <= tol, f"{cfg.name}: rel err {err:.3e} > {tol}"
+    if cfg.model == "sage":   # end to end: the oracle chains its own fp64 H1 (A19)
+        ref_e2e = H.oracle_step(oracle, cfg, og, d, rows=rows)[1]
+        yy = H.to_np(outs[1] if rows is None else outs[1][torch.from_numpy(rows).to(DEV)])
+        assert oracle.rel_err(yy, ref_e2e) <= tol
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+def test_config_full(saga, cfg):
+    _config_check(saga, W.CONFIGS[cfg])
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_config_scaled_ragged(saga, cfg):
+    """Same recipe at a size that is not a multiple of any tile (ragged tails)."""
+    c = W.CONFIGS[cfg]
+    _config_check(saga, W.scaled(c, 3000 if cfg != "C5" else 5000, 40000, cfg + "r"))
+
+
+def test_c5_full_sampled(saga):
+    """C5 at full size (launch config the bench times), sampled rows incl. hubs."""
+    _config_check(saga, W.CONFIGS["C5"], rows_k=3000)
+
+
+def test_relabel_invariance_gpu(saga):
+    cfg = W.scaled(W.CONFIGS["C3"], 2000, 30000, "rl")
+    d = W.make_inputs(cfg, "cpu")
+    perm = torch.randperm(cfg.n, generator=torch.Generator().manual_seed(1)).to(torch.int32)
+    d2 = dict(d)
+    d2["src"], d2["dst"] = perm[d["src"].long()], perm[d["dst"].long()]
+    X2 = torch.empty_like(d["X"])
+    X2[perm.long()] = d["X"]
+    d2["X"] = X2
+    a, b = H.dev_inputs(d, DEV), H.dev_inputs(d2, DEV)
+    ya = H.gpu_step(__import__("paper_2009_00804_b200"), cfg, H.gpu_graph(saga, cfg, a), a)[0][0]
+    yb = H.gpu_step(saga, cfg, H.gpu_graph(saga, cfg, b), b)[0][0]
+    err = oracle.rel_err(H.to_np(yb[perm.long().to(DEV)]), H.to_np(ya))
+    assert err <= 2e-2
