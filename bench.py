@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""bench.py -- one SAGA-NN layer at inference on B200 (arXiv 2009.00804).
+
+Metric (BASELINE.json): ms/layer and edge-feature updates/s per SAGA-NN layer;
+% of HBM roofline.  A "step" is one pass of the whole hot path over one batch
+(SURVEY.md 8(a) rows S1-S6 on a pre-built graph: pre-projection GEMM, fused
+Scatter/ApplyEdge/Gather, ApplyVertex epilogue).  S0 (graph build) runs once
+per graph and is reported separately (and inside the `e2e` figure).
+
+Default workload: config C5 (GCN at scale, R-MAT 2^22 vertices, 2^26 edges +
+self-loops, 256 -> 256 bf16), the largest configuration (BASELINE.json
+configs[4]); C1-C4 are parity-test cases (`--config` runs them too).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl saga|reference]
+
+N > 1 (torchrun): one independent replica per GPU ("replicas only": the
+north star fixes one GPU with no sharding), value = total updates / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "edge-feature updates/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"],
+                "bf16_tflops_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- byte model ----
+def algorithmic(cfg):
+    """Algorithmic (compulsory) bytes and FLOPs per launch of each kernel
+    (DESIGN.md "Roofline"): every array the kernel must touch, once."""
+    n, e = cfg.n, cfg.num_edges
+    out = {}
+    if cfg.model == "gcn" and cfg.dtype == "bf16":
+        fi, fo = cfg.dims
+        out["gemm_bf16_tc"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * 4 + n * fo * 2, "flops": 2 * n * fi * fo}
+        out["agg_gcn_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 4 + n * fo * 2, "flops": e * fo}
+    elif cfg.model == "gcn":
+        fi, fo = cfg.dims
+        out["gcn_f32_fused"] = {"bytes": e * 4 + (n + 1) * 8 + n * fi * 4 + n * 4 + n * fo * 4,
+                                "flops": 2 * e * fi + 2 * n * fi * fo}
+    elif cfg.model == "sage":
+        f0, f1, f2 = cfg.dims
+        out["agg_mean_bf16"] = {"bytes": 2 * (e * 4 + (n + 1) * 8) + n * (f0 + f1) * 2 * 2, "flops": e * (f0 + f1)}
+        out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f0 + f1 + 2 * f1 + f2), "flops": 2 * n * (2 * f0 * f1 + 2 * f1 * f2)}
+    elif cfg.model == "gat":
+        fi, fo = cfg.dims
+        out["gemm_bf16_tc_gat"] = {"bytes": n * fi * 2 + n * fo * 2 + n * 64, "flops": 2 * n * fi * fo}
+        out["gat_edge"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 64 + n * fo * 2, "flops": 10 * e * fo}
+    elif cfg.model == "gated":
+        f = cfg.dims[0]
+        out["agg_typed_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f}
+        out["gated_apply_sgemm"] = {"bytes": n * 4 * f * 4 + n * f * 4 * 3, "flops": 2 * n * (4 * f * f + 6 * f * f)}
+    return out
+
+
+# --------------------------------------------------------------- helpers ----
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def emit(obj, rank):
+    if rank == 0:
+        print(json.dumps(obj), flush=True)
+
+
+def l2_flush_buffer(dev):
+    return torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+
+def cpu_baseline(cfg, d_cpu, og, sample_rows, oracle):
+    """Time the oracle (as it stands) on a bounded row sample on host cores."""
+    t0 = time.perf_counter()
+    harness_step_rows(cfg, og, d_cpu, sample_rows, oracle)
+    dt = time.perf_counter() - t0
+    upd = sample_updates(cfg, og, sample_rows)
+    return upd / dt, dt, upd
+
+
+def harness_step_rows(cfg, og, c, rows, oracle):
+    """The oracle's configured step restricted to destination `rows`
+    (SAGE: both layers over all rows -- layer 2 needs H1 of every neighbour)."""
+    if cfg.model == "gcn":
+        return oracle.gcn(og, c["X"], c["W"].float(), c["b"], act=1, rows=rows)
+    if cfg.model == "sage":
+        h1 = oracle.sage_mean(og, c["X"], c["W1"].float(), act=1)
+        return oracle.sage_mean(og, h1, c["W2"].float(), act=0)
+    if cfg.model == "gat":
+        return oracle.gat(og, c["X"], c["W"].float(), c["a_src"], c["a_dst"], 0.2, rows=rows)
+    return oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)
+
+
+def sample_updates(cfg, og, rows):
+    if cfg.model == "sage":
+        return cfg.layer_updates()
+    deg = og.in_deg[np.asarray(rows)].astype(np.int64).sum()
+    return int(deg) * cfg.f_canon
+
+
+def pick_sample(og, target_edges, seed=1):
+    rng = np.random.default_rng(seed)
+    rows = rng.permutation(og.n)
+    cum = np.cumsum(og.in_deg[rows].astype(np.int64))
+    k = int(np.searchsorted(cum, target_edges)) + 1
+    return np.sort(rows[:k]).astype(np.int64)
+
+
+def oracle_threads():
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
+# ------------------------------------------------------------ reference ----
+def run_reference(args, cfg):
+    """--impl reference: the fp64 oracle as it stands on the host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    d = W.make_inputs(cfg, dev)
+    c = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in d.items()}
+    og = oracle.csr_build(cfg.n, c["src"], c["dst"], c.get("etype"), cfg.num_etypes)
+    rows = pick_sample(og, args.ref_edges)
+    for _ in range(args.warmup):
+        harness_step_rows(cfg, og, c, rows[: max(1, len(rows) // 8)], oracle)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        harness_step_rows(cfg, og, c, rows, oracle)
+        times.append(time.perf_counter() - t0)
+    upd = sample_updates(cfg, og, rows)
+    tot = sum(times)
+    val = upd * args.steps / tot
+    cores = oracle_threads()
+    sample = f"{len(rows)} destination rows ({upd // cfg.f_canon} in-edges) of {cfg.name} per step, fp64 C oracle"
+    emit({"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+          "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+          "config": workload_config(cfg),
+          "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+          "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}, 0)
+
+
+def workload_config(cfg):
+    desc = {"C1": "GCN fp32, ER N=2048 E=10240+self-loops, 64->16",
+            "C2": "GraphSAGE-mean x2 bf16, R-MAT N=2^16 E=2^20 distinct, 128->128->64",
+            "C3": "GAT 8x8 heads bf16, R-MAT N=2^18 E=2^22+self-loops, 256->64",
+            "C4": "gated GRU fp32, R-MAT N=2^17 E=2^21, 4 edge types, 128",
+            "C5": "GCN at scale bf16, R-MAT N=2^22 E=2^26+self-loops, 256->256"}
+    return {"workload": f"{cfg.name}: {desc.get(cfg.name, cfg.name)}", "vertices": cfg.n, "edges": cfg.num_edges,
+            "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
+
+
+# ----------------------------------------------------------------- main ----
+def run_saga(args, cfg):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2009_00804_b200 as saga
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from tests import harness as H
+
+    d = W.make_inputs(cfg, dev)
+    torch.cuda.synchronize()
+    # S0 graph build (once per graph; timed separately)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    g = H.gpu_graph(saga, cfg, d)
+    t1.record()
+    torch.cuda.synchronize()
+    build_ms = t0.elapsed_time(t1)
+
+    outs, layers = H.gpu_step(saga, cfg, g, d)
+    big = cfg.n * max(cfg.dims) * (2 if cfg.dtype == "bf16" else 4) > (256 << 20)
+    flush = None if big else l2_flush_buffer(dev)
+    for _ in range(args.warmup):
+        H.gpu_step(saga, cfg, g, d, layers)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.15)
+    saga.saga_profile_enable(True)
+    for i in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        starts[i].record(stream)
+        H.gpu_step(saga, cfg, g, d, layers)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    prof = saga.saga_profile_read()
+    saga.saga_profile_enable(False)
+    clocks = clk.stop()
+    if ws > 1:
+        torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    upd_step = cfg.layer_updates()
+    value = upd_step * args.steps * ws / (tot_ms / 1e3)
+    launches = sum(n for n, _ in prof.values())
+
+    # roofline of the dominant kernel
+    alg = algorithmic(cfg)
+    pk = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    roof = None
+    if dom:
+        n_l, ms_l = prof[dom]
+        avg_s = ms_l / n_l / 1e3
+        a = alg.get(dom, {"bytes": 0, "flops": 0})
+        bound = "tensor" if dom.startswith("gemm") and a["flops"] / max(a["bytes"], 1) > \
+            pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9) else "hbm"
+        if bound == "hbm":
+            ach = a["bytes"] / avg_s / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / pk["hbm_gbs"], "traffic": args.traffic, "kernel": dom,
+                    "kernel_ms": avg_s * 1e3, "algorithmic_bytes": a["bytes"], "peak_source": pk["source"]}
+        else:
+            ach = a["flops"] / avg_s / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                    "frac": ach / pk["bf16_tflops"], "traffic": args.traffic, "kernel": dom,
+                    "kernel_ms": avg_s * 1e3, "peak_source": pk["source"]}
+    kernels = {}
+    for k, (n_l, ms_l) in prof.items():
+        a = alg.get(k, {"bytes": 0, "flops": 0})
+        avg = ms_l / n_l
+        kernels[k] = {"launches": n_l, "avg_ms": avg, "share": ms_l / tot_ms if ws == 1 else None,
+                      "alg_GBps": a["bytes"] / (avg / 1e3) / 1e9, "alg_TFLOPs": a["flops"] / (avg / 1e3) / 1e12}
+
+    # end to end through the public API with host buffers
+    e2e = run_e2e(args, cfg, saga, H, d, dev, ws) if args.e2e_steps > 0 else None
+
+    # CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle
+        c = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in d.items()}
+        og = oracle.csr_build(cfg.n, c["src"], c["dst"], c.get("etype"), cfg.num_etypes)
+        rows = pick_sample(og, args.ref_edges)
+        v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+               "sample": f"{len(rows)} random destination rows of {cfg.name} ({upd // cfg.f_canon} in-edges), "
+                         f"fp64 C oracle, {dt:.1f} s"}
+
+    conf = workload_config(cfg)
+    conf.update({"l2": "inputs larger than L2 (no flush)" if big else "512 MiB L2 flush between steps (untimed)",
+                 "graph_build_ms": build_ms, "per_kernel": kernels})
+    res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
+           "data": "synthetic (seeded counter-based generator, workloads/)", "config": conf,
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+    emit(res, rank)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(args, cfg, saga, H, d, dev, ws):
+    """Same metric through the public API with HOST inputs: per step, H2D of
+    the COO + features from pinned memory, saga_graph_build, the layer step,
+    D2H of the output; all inside the timed region."""
+    feats = [k for k in ("X", "H") if k in d]
+    host = {k: v.cpu().pin_memory() for k, v in d.items() if isinstance(v, torch.Tensor)}
+    h2d = sum(host[k].numel() * host[k].element_size() for k in ("src", "dst") + tuple(feats))
+    if "etype" in host and host["etype"] is not None:
+        h2d += host["etype"].numel() * 4
+    weights_dev = {k: v for k, v in d.items() if k not in ("src", "dst", "etype", "X", "H")}
+    out_host = None
+    times = []
+    for it in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dd = dict(weights_dev)
+        for k in ("src", "dst", "etype") + tuple(feats):
+            if k in host and host[k] is not None:
+                dd[k] = host[k].to(dev, non_blocking=True)
+        dd.setdefault("etype", None)
+        g = H.gpu_graph(saga, cfg, dd)
+        outs, _ = H.gpu_step(saga, cfg, g, dd)
+        if out_host is None:
+            out_host = torch.empty(outs[-1].shape, dtype=outs[-1].dtype, pin_memory=True)
+        out_host.copy_(outs[-1], non_blocking=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        g.close()
+        if it > 0:   # first iteration is warm-up
+            times.append(dt)
+    d2h = out_host.numel() * out_host.element_size()
+    tmax = sum(times)
+    if ws > 1:
+        t = torch.tensor([tmax], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tmax = float(t.item())
+    return {"value": cfg.layer_updates() * len(times) * ws / tmax, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * tmax / len(times),
+            "includes": "H2D COO+features, saga_graph_build, layer, D2H output"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-edges", type=int, default=2_000_000,
+                    help="in-edges per oracle sample (bounded CPU work)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/), if known")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3   # timing rule: >= 3 warm-up steps
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_saga(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

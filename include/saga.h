@@ -182,6 +182,18 @@ SAGA_API saga_status saga_layer(saga_model kind, const saga_graph *g, const saga
 /* Release a graph (stream-ordered on the stream it was built on). NULL-safe. */
 SAGA_API void saga_free(saga_graph *g);
 
+/*
+ * Optional per-kernel timing (tracing).  When enabled (process-wide), every
+ * kernel saga_layer launches is bracketed by a CUDA event pair recorded on
+ * the caller's stream; saga_profile_get synchronises those events and
+ * returns, per kernel name, the launch count and the summed device time in
+ * milliseconds since the last saga_profile_enable call (which resets).
+ * Costs two event records per launch; disabled by default.
+ */
+SAGA_API saga_status saga_profile_enable(int enable);
+SAGA_API int32_t saga_profile_count(void);
+SAGA_API saga_status saga_profile_get(int32_t index, const char **name, int64_t *launches, double *total_ms);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 SAGA_API const char *saga_last_error(void);
 

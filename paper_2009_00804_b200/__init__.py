@@ -29,7 +29,8 @@ MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GAT
 
 # Every symbol include/saga.h declares (checked by tests/test_abi.py).
 EXPORTS = ["saga_abi_version", "saga_graph_build", "saga_graph_info", "saga_graph_copy_csr",
-           "saga_layer_workspace_bytes", "saga_layer", "saga_free", "saga_last_error"]
+           "saga_layer_workspace_bytes", "saga_layer", "saga_free", "saga_last_error",
+           "saga_profile_enable", "saga_profile_count", "saga_profile_get"]
 
 
 class SagaError(RuntimeError):
@@ -78,6 +79,13 @@ def _load():
     L.saga_free.argtypes = [P]
     L.saga_last_error.restype = ctypes.c_char_p
     L.saga_last_error.argtypes = []
+    L.saga_profile_enable.restype = ctypes.c_int
+    L.saga_profile_enable.argtypes = [ctypes.c_int]
+    L.saga_profile_count.restype = ctypes.c_int32
+    L.saga_profile_count.argtypes = []
+    L.saga_profile_get.restype = ctypes.c_int
+    L.saga_profile_get.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64),
+                                   ctypes.POINTER(ctypes.c_double)]
     return L
 
 
@@ -86,6 +94,21 @@ _lib = _load()
 
 def saga_abi_version() -> int:
     return _lib.saga_abi_version()
+
+
+def saga_profile_enable(enable: bool = True):
+    """Per-kernel CUDA-event timing inside saga_layer (resets the counters)."""
+    _check(_lib.saga_profile_enable(1 if enable else 0))
+
+
+def saga_profile_read() -> dict:
+    """{kernel name: (launches, total device ms)} since the last enable."""
+    out = {}
+    for i in range(_lib.saga_profile_count()):
+        name, n, ms = ctypes.c_char_p(), ctypes.c_int64(), ctypes.c_double()
+        _check(_lib.saga_profile_get(i, ctypes.byref(name), ctypes.byref(n), ctypes.byref(ms)))
+        out[name.value.decode()] = (n.value, ms.value)
+    return out
 
 
 def saga_last_error() -> str:

@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -37,6 +39,74 @@ saga_status cuda_fail(cudaError_t e, const char *what) {
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ------------------------------------------------------------ profiling ----
+struct ProfRec {
+    int name;
+    cudaEvent_t a, b;
+};
+struct Prof {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::string> names;
+    std::vector<int64_t> launches;
+    std::vector<double> ms;
+    std::vector<ProfRec> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    int id(const char *n) {
+        for (size_t i = 0; i < names.size(); ++i)
+            if (names[i] == n) return (int)i;
+        names.emplace_back(n);
+        launches.push_back(0);
+        ms.push_back(0.0);
+        return (int)names.size() - 1;
+    }
+    void drain() {
+        for (auto &r : pending) {
+            cudaEventSynchronize(r.b);
+            float t = 0.f;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            ms[r.name] += t;
+            launches[r.name] += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+};
+Prof g_prof;
+
+// RAII bracket around one kernel launch (no-op unless profiling is on).
+struct ProfScope {
+    bool on;
+    ProfRec r{};
+    cudaStream_t st;
+    ProfScope(const char *name, cudaStream_t s) : on(false), st(s) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        if (!g_prof.on) return;
+        on = true;
+        r.name = g_prof.id(name);
+        r.a = g_prof.get();
+        r.b = g_prof.get();
+        cudaEventRecord(r.a, st);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.b, st);
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.pending.push_back(r);
+    }
+};
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -157,6 +227,30 @@ saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g, con
     return SAGA_OK;
 }
 
+saga_status saga_profile_enable(int enable) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.drain();
+    g_prof.on = enable != 0;
+    std::fill(g_prof.launches.begin(), g_prof.launches.end(), 0);
+    std::fill(g_prof.ms.begin(), g_prof.ms.end(), 0.0);
+    return SAGA_OK;
+}
+
+int32_t saga_profile_count(void) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    return (int32_t)g_prof.names.size();
+}
+
+saga_status saga_profile_get(int32_t index, const char **name, int64_t *launches, double *total_ms) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.drain();
+    if (index < 0 || index >= (int32_t)g_prof.names.size()) return fail(SAGA_EINVAL, "profile index out of range");
+    if (name) *name = g_prof.names[index].c_str();
+    if (launches) *launches = g_prof.launches[index];
+    if (total_ms) *total_ms = g_prof.ms[index];
+    return SAGA_OK;
+}
+
 void saga_free(saga_graph *g) {
     if (!g) return;
     saga::free_graph(&g->d);
@@ -205,9 +299,12 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 if (!(o.in_dim == 16 || o.in_dim == 32 || o.in_dim == 64 || o.in_dim == 128) || o.out_dim < 1 ||
                     o.out_dim > 64)
                     return fail(SAGA_EUNSUPPORTED, "fp32 GCN supports in_dim in {16,32,64,128}, out_dim <= 64");
+                {
+                ProfScope ps_("gcn_f32_fused", st);
                 e = launch_gcn_f32_fused(d, static_cast<const float *>(x->data), o.in_dim,
                                          static_cast<const float *>(w->W), o.out_dim, w->bias, o.act,
                                          static_cast<float *>(out->data), aw, st);
+            }
                 if (e) return cuda_fail(e, "gcn_f32_fused");
                 return SAGA_OK;
             }
@@ -224,9 +321,15 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.out = Y;
             a.epi = EPI_ROWSCALE;
             a.row_scale = d.dinv;
-            e = launch_gemm_bf16_tc(a, st, &why);
+            {
+                ProfScope ps_("gemm_bf16_tc", st);
+                e = launch_gemm_bf16_tc(a, st, &why);
+            }
             if (e) return fail(SAGA_ECUDA, "gcn gemm: %s (%s)", cudaGetErrorString(e), why);
-            e = launch_agg_gcn_bf16(d, Y, o.out_dim, w->bias, o.act, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            {
+                ProfScope ps_("agg_gcn_bf16", st);
+                e = launch_agg_gcn_bf16(d, Y, o.out_dim, w->bias, o.act, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            }
             if (e) return cuda_fail(e, "gcn aggregate");
             return SAGA_OK;
         }
@@ -237,7 +340,10 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 return fail(SAGA_EUNSUPPORTED, "SAGE supports in_dim in {64,128}, out_dim in {64,128,256}");
             if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE act must be NONE/RELU");
             __nv_bfloat16 *M = reinterpret_cast<__nv_bfloat16 *>(i0);
-            e = launch_agg_mean_bf16(d, static_cast<const __nv_bfloat16 *>(x->data), o.in_dim, M, aw, st);
+            {
+                ProfScope ps_("agg_mean_bf16", st);
+                e = launch_agg_mean_bf16(d, static_cast<const __nv_bfloat16 *>(x->data), o.in_dim, M, aw, st);
+            }
             if (e) return cuda_fail(e, "sage aggregate");
             GemmArgs a;
             a.M = d.n; a.K0 = o.in_dim; a.K1 = o.in_dim; a.N = o.out_dim;
@@ -248,7 +354,10 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.epi = EPI_BIAS_ACT;
             a.bias = w->bias;
             a.act = o.act;
-            e = launch_gemm_bf16_tc(a, st, &why);
+            {
+                ProfScope ps_("gemm_bf16_tc", st);
+                e = launch_gemm_bf16_tc(a, st, &why);
+            }
             if (e) return fail(SAGA_ECUDA, "sage gemm: %s (%s)", cudaGetErrorString(e), why);
             return SAGA_OK;
         }
@@ -267,9 +376,15 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.out = z;
             a.epi = EPI_GAT;
             a.a_src = w->attn_src; a.a_dst = w->attn_dst; a.el = el; a.er = er;
-            e = launch_gemm_bf16_tc(a, st, &why);
+            {
+                ProfScope ps_("gemm_bf16_tc_gat", st);
+                e = launch_gemm_bf16_tc(a, st, &why);
+            }
             if (e) return fail(SAGA_ECUDA, "gat gemm: %s (%s)", cudaGetErrorString(e), why);
-            e = launch_gat_edge(d, z, el, er, o.leaky_slope, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            {
+                ProfScope ps_("gat_edge", st);
+                e = launch_gat_edge(d, z, el, er, o.leaky_slope, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+            }
             if (e) return cuda_fail(e, "gat edge");
             return SAGA_OK;
         }
@@ -280,10 +395,16 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (!w->W_type || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
                 return fail(SAGA_EINVAL, "GATED needs W_type, W_ih, W_hh, b_ih, b_hh");
             float *S = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
-            e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, aw, st);
+            {
+                ProfScope ps_("agg_typed_f32", st);
+                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, aw, st);
+            }
             if (e) return cuda_fail(e, "typed aggregate");
-            e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
+            {
+                ProfScope ps_("gated_apply_sgemm", st);
+                e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
                                    w->W_ih, w->W_hh, w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
+            }
             if (e) return cuda_fail(e, "gated apply");
             return SAGA_OK;
         }
