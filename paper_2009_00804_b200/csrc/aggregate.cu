@@ -4,21 +4,36 @@
 // Paper: the Gather stage reduces each vertex's in-edges (PAPER.md lines
 // 343-355); fused with Scatter it is "the multiplication between the
 // adjacency matrix and the embedding matrix" (line 354) -- the SpMM shape,
-// which is HBM-bound on B200 (~0 FLOP/byte).  Power-law in-degrees (lines
+// which is HBM/L2-bound on B200 (~0 FLOP/byte).  Power-law in-degrees (lines
 // 359-365) make per-vertex scheduling unbalanced, so work is cut by
 // merge-path: the item sequence is, for every row v in order, its deg(v)
 // edges followed by one row-end marker; task k owns items [kT, (k+1)T).
-// A group of G lanes (16 bytes of the row per lane) streams its task's
-// col_src in coalesced chunks, keeps U independent 16-byte row gathers in
-// flight, and flushes a row (epilogue + coalesced store) at each row end.
+//
+// One WARP owns one task, so every branch below is warp-uniform:
+//  * G lanes cover one feature row (16 bytes per lane); the warp's S = 32/G
+//    sub-groups take S different in-edges of the same row per step, and a
+//    batch is U steps = U*S edges of ONE row (a batch never crosses a row
+//    end, so the reduction needs no per-edge row test); the U*S 16-byte row
+//    gathers of a batch are all issued before any is consumed;
+//  * col_src (and etype) arrive in coalesced 32-edge chunks, one ahead;
+//  * row_end and per-row epilogue data (dinv[v], GAT er[v,:]) come from
+//    32-lane register windows refilled once per 32 rows;
+//  * at a row end the S sub-group partials are combined with xor-shuffles
+//    and sub-group 0 runs the fused epilogue and the coalesced store.
+// Feature rows are read with plain ld.global.nc (L2 evict-normal): the hot
+// (high out-degree) rows then stay in the 126 MB L2 -- an L1::no_allocate
+// load is treated as evict-first by L2 and cost ~45% in a probe
+// (scripts/gather_probe.cu).  bf16 rows are accumulated with sm_100's
+// mixed-precision add (add.f32.bf16: one FHADD per element, no unpacking).
 // Rows split across tasks (hubs, and rows straddling a task boundary) write
-// fp32 partials; the last contributor (atomic ticket) merges all partials in
+// fp32 partials; the last contributor (integer ticket) merges all partials in
 // task order, so results are deterministic and no float atomics are used.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -27,6 +42,8 @@ namespace saga {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int kWarpsPerBlock = kBlock / 32;
+constexpr uint32_t kFull = 0xffffffffu;
 
 struct GraphView {
     const int64_t *row_ptr;
@@ -36,36 +53,11 @@ struct GraphView {
     const int64_t *task_p;
     int64_t T, ntasks;
     int32_t n;
+    int32_t e;
 };
 
 GraphView view(const GraphDev &g) {
-    return GraphView{g.row_ptr, g.col_src, g.etype, g.task_v, g.task_p, g.task_items, g.ntasks, g.n};
-}
-
-template <int G>
-struct Group {
-    int lane;       // lane within the group
-    uint32_t mask;  // warp mask of the group
-    __device__ Group() {
-        const int wl = threadIdx.x & 31;
-        lane = wl & (G - 1);
-        mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (wl & ~(G - 1)));
-    }
-    template <typename V>
-    __device__ __forceinline__ V shfl(V v, int src) const {
-        return __shfl_sync(mask, v, src, G);
-    }
-    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
-};
-
-__device__ __forceinline__ void add_bf16x8(float (&a)[8], const uint4 &u, float w = 1.0f) {
-    const uint32_t q[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        float2 f = ptx::unpack_bf16x2(q[i]);
-        a[2 * i] = fmaf(w, f.x, a[2 * i]);
-        a[2 * i + 1] = fmaf(w, f.y, a[2 * i + 1]);
-    }
+    return GraphView{g.row_ptr, g.col_src, g.etype, g.task_v, g.task_p, g.task_items, g.ntasks, g.n, (int32_t)g.e};
 }
 
 __device__ __forceinline__ uint4 pack8(const float (&o)[8]) {
@@ -80,219 +72,229 @@ __device__ __forceinline__ float act_fn(float x, int act) {
 }
 
 // ===================================================================== ops ==
+// Op interface (all const; per-row state is the float `rs` the engine fetches
+// from its window: kWin values per row, lane gl % kWin's one):
+//   Acc, Val; kWin; row_value(v, j)
+//   zero(acc); load(u, gl); add(acc, val, rs, t); reduce_xor(acc, offset)
+//   finish(v, acc, rs, gl, store)  [or finish_w: warp-wide epilogue]
+//   save(slot, acc, gl); merge(acc, slot, gl)
+
 // Sum of bf16 rows (8 per lane) -> act(scale[v] * acc + bias) in bf16.
 // GCN (Y pre-scaled by dinv[u], scale = dinv[v]) and SAGE-mean (scale = 1/deg).
+template <int kAct>
 struct SumBf16Op {
-    __device__ void set_smem(const float *) {}
-    static constexpr int kAccF = 8;
+    static constexpr int kWin = 1;
     struct Acc { float a[8]; };
     struct Val { uint4 x; };
     const __nv_bfloat16 *X;
     int32_t f;
     const float *scale;
     const float *bias;
-    int act;
     __nv_bfloat16 *out;
-    __device__ void setup(int) {}
+    __device__ __forceinline__ float row_value(int32_t v, int) const { return __ldg(scale + v); }
     __device__ __forceinline__ void zero(Acc &c) const {
 #pragma unroll
         for (int i = 0; i < 8; ++i) c.a[i] = 0.0f;
     }
-    __device__ __forceinline__ void begin_row(int32_t, int) {}
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        return Val{ptx::ldg_nc_v4(X + (int64_t)u * f + lane * 8)};
+    __device__ __forceinline__ Val load(int32_t u, int gl) const {
+        return Val{__ldg(reinterpret_cast<const uint4 *>(X + (int64_t)u * f) + gl)};
     }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, int32_t) const { add_bf16x8(c.a, v.x); }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, int lane) const {
-        const float s = scale[v];
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t) const {
+        ptx::add_bf16x2_f32(c.a[0], c.a[1], v.x.x);
+        ptx::add_bf16x2_f32(c.a[2], c.a[3], v.x.y);
+        ptx::add_bf16x2_f32(c.a[4], c.a[5], v.x.z);
+        ptx::add_bf16x2_f32(c.a[6], c.a[7], v.x.w);
+    }
+    __device__ __forceinline__ void reduce_xor(Acc &c, int o) const {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c.a[i] += __shfl_xor_sync(kFull, c.a[i], o);
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float rs, int gl, bool store) const {
         float b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (bias) {
-            const float4 *bp = reinterpret_cast<const float4 *>(bias + lane * 8);
-            float4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
+            const float4 *bp = reinterpret_cast<const float4 *>(bias + gl * 8);
+            const float4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
             b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
             b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
         }
         float o[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = act_fn(fmaf(s, c.a[i], b[i]), act);
-        *reinterpret_cast<uint4 *>(out + (int64_t)v * f + lane * 8) = pack8(o);
+        for (int i = 0; i < 8; ++i) o[i] = act_fn(fmaf(rs, c.a[i], b[i]), kAct);
+        if (store) *reinterpret_cast<uint4 *>(out + (int64_t)v * f + gl * 8) = pack8(o);
     }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
-        float4 *p = reinterpret_cast<float4 *>(slot + lane * 8);
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int gl) const {
+        float4 *p = reinterpret_cast<float4 *>(slot + gl * 8);
         p[0] = make_float4(c.a[0], c.a[1], c.a[2], c.a[3]);
         p[1] = make_float4(c.a[4], c.a[5], c.a[6], c.a[7]);
     }
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
-        const float4 *p = reinterpret_cast<const float4 *>(slot + lane * 8);
-        float4 x = __ldcg(p), y = __ldcg(p + 1);
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int gl) const {
+        const float4 *p = reinterpret_cast<const float4 *>(slot + gl * 8);
+        const float4 x = __ldcg(p), y = __ldcg(p + 1);
         c.a[0] += x.x; c.a[1] += x.y; c.a[2] += x.z; c.a[3] += x.w;
         c.a[4] += y.x; c.a[5] += y.y; c.a[6] += y.z; c.a[7] += y.w;
     }
 };
 
 // C1: fp32 rows (4 per lane), weight dinv[u] per edge, then the ApplyVertex
-// GEMV (W staged in shared memory) fused into the row flush.
+// GEMV (W staged in shared memory) fused into the row flush, spread over all
+// 32 lanes (lane L computes outputs L and L + 32).
 struct GcnF32FusedOp {
-    static constexpr int kAccF = 4;
+    static constexpr int kWin = 1;
     struct Acc { float a[4]; };
     struct Val { float4 x; float w; };
     const float *X;
     int32_t f_in, f_out;
     const float *dinv;
-    const float *W;  // global [f_in][f_out]
     const float *bias;
     int act;
     float *out;
-    const float *Ws;  // shared copy (set by the engine)
-    __device__ void setup(int) {}
-    __device__ void set_smem(const float *p) { Ws = p; }
+    __device__ __forceinline__ float row_value(int32_t v, int) const { return __ldg(dinv + v); }
     __device__ __forceinline__ void zero(Acc &c) const { c.a[0] = c.a[1] = c.a[2] = c.a[3] = 0.0f; }
-    __device__ __forceinline__ void begin_row(int32_t, int) {}
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
+    __device__ __forceinline__ Val load(int32_t u, int gl) const {
         Val v;
-        v.x = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)u * f_in) + lane);
+        v.x = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)u * f_in) + gl);
         v.w = __ldg(dinv + u);
         return v;
     }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, int32_t) const {
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t) const {
         c.a[0] = fmaf(v.w, v.x.x, c.a[0]);
         c.a[1] = fmaf(v.w, v.x.y, c.a[1]);
         c.a[2] = fmaf(v.w, v.x.z, c.a[2]);
         c.a[3] = fmaf(v.w, v.x.w, c.a[3]);
     }
-    template <int G>
-    __device__ __forceinline__ void finish_g(int32_t v, const Acc &c, const Group<G> &grp) const {
-        const float s = dinv[v];
-        float h[4] = {s * c.a[0], s * c.a[1], s * c.a[2], s * c.a[3]};
-        // lane j computes outputs j, j+G, ...: out_j = sum_k h_k W[k][j]
-        constexpr int kMaxOut = 64 / G > 0 ? (64 + G - 1) / G : 1;
-        float o[kMaxOut];
+    __device__ __forceinline__ void reduce_xor(Acc &c, int o) const {
 #pragma unroll
-        for (int t = 0; t < kMaxOut; ++t) o[t] = 0.0f;
+        for (int i = 0; i < 4; ++i) c.a[i] += __shfl_xor_sync(kFull, c.a[i], o);
+    }
+    // h = rs * acc lives in lanes 0..f_in/4-1 (4 values each, sub-group 0)
+    __device__ __forceinline__ void finish_w(int32_t v, const Acc &c, float rs, const float *Ws, int lane) const {
+        const float h[4] = {rs * c.a[0], rs * c.a[1], rs * c.a[2], rs * c.a[3]};
+        float o0 = 0.0f, o1 = 0.0f;
+        const int j0 = lane, j1 = lane + 32;
         for (int k4 = 0; k4 < f_in / 4; ++k4) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                float hk = grp.shfl(h[i], k4);
+                const float hk = __shfl_sync(kFull, h[i], k4);
                 const float *wr = Ws + (k4 * 4 + i) * f_out;
-#pragma unroll
-                for (int t = 0; t < kMaxOut; ++t) {
-                    int j = grp.lane + t * G;
-                    if (j < f_out) o[t] = fmaf(hk, wr[j], o[t]);
-                }
+                if (j0 < f_out) o0 = fmaf(hk, wr[j0], o0);
+                if (j1 < f_out) o1 = fmaf(hk, wr[j1], o1);
             }
         }
-#pragma unroll
-        for (int t = 0; t < kMaxOut; ++t) {
-            int j = grp.lane + t * G;
-            if (j < f_out) out[(int64_t)v * f_out + j] = act_fn(o[t] + (bias ? bias[j] : 0.0f), act);
-        }
+        if (j0 < f_out) out[(int64_t)v * f_out + j0] = act_fn(o0 + (bias ? __ldg(bias + j0) : 0.0f), act);
+        if (j1 < f_out) out[(int64_t)v * f_out + j1] = act_fn(o1 + (bias ? __ldg(bias + j1) : 0.0f), act);
     }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
-        reinterpret_cast<float4 *>(slot)[lane] = make_float4(c.a[0], c.a[1], c.a[2], c.a[3]);
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int gl) const {
+        reinterpret_cast<float4 *>(slot)[gl] = make_float4(c.a[0], c.a[1], c.a[2], c.a[3]);
     }
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
-        float4 x = __ldcg(reinterpret_cast<const float4 *>(slot) + lane);
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int gl) const {
+        const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot) + gl);
         c.a[0] += x.x; c.a[1] += x.y; c.a[2] += x.z; c.a[3] += x.w;
     }
 };
 
-// C3: GAT.  Lane = head (8 bf16 = head_dim 8 = 16 bytes of z).  Per edge:
+// C3: GAT.  Lane gl = head (8 bf16 = head_dim 8 = 16 bytes of z).  Per edge:
 // s = LeakyReLU(el[u,h] + er[v,h]) (additive form of a^T[z_u||z_v], A14);
 // online softmax state (m, l, acc[8]) per head; flush ELU(acc / l).
+// Row value: er[v, gl] (kWin = 8 heads).
 struct GatOp {
-    __device__ void set_smem(const float *) {}
-    static constexpr int kAccF = 10;
+    static constexpr int kWin = 8;
     struct Acc { float m, l, a[8]; };
     struct Val { uint4 z; float el; };
     const __nv_bfloat16 *z;
     const float *el, *er;
     float slope;
     __nv_bfloat16 *out;
-    float er_h;
-    __device__ void setup(int) {}
+    __device__ __forceinline__ float row_value(int32_t v, int j) const { return __ldg(er + (int64_t)v * 8 + j); }
     __device__ __forceinline__ void zero(Acc &c) const {
         c.m = -INFINITY;
         c.l = 0.0f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) c.a[i] = 0.0f;
     }
-    __device__ __forceinline__ void begin_row(int32_t v, int lane) { er_h = __ldg(er + (int64_t)v * 8 + lane); }
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
+    __device__ __forceinline__ Val load(int32_t u, int gl) const {
         Val v;
-        v.z = ptx::ldg_nc_v4(z + (int64_t)u * 64 + lane * 8);
-        v.el = __ldg(el + (int64_t)u * 8 + lane);
+        v.z = __ldg(reinterpret_cast<const uint4 *>(z + (int64_t)u * 64) + gl);
+        v.el = __ldg(el + (int64_t)u * 8 + gl);
         return v;
     }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, int32_t) const {
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h, int32_t) const {
         float s = v.el + er_h;
         s = s > 0.0f ? s : slope * s;
-        float mn = fmaxf(c.m, s);
-        float co = __expf(c.m - mn);  // 0 when c.m = -inf
-        float cn = __expf(s - mn);
+        const float mn = fmaxf(c.m, s);
+        const float co = __expf(c.m - mn);  // 0 when c.m = -inf
+        const float cn = __expf(s - mn);
         c.l = fmaf(c.l, co, cn);
         const uint32_t q[4] = {v.z.x, v.z.y, v.z.z, v.z.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            float2 f = ptx::unpack_bf16x2(q[i]);
+            const float2 f = ptx::unpack_bf16x2(q[i]);
             c.a[2 * i] = fmaf(c.a[2 * i], co, cn * f.x);
             c.a[2 * i + 1] = fmaf(c.a[2 * i + 1], co, cn * f.y);
         }
         c.m = mn;
     }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, int lane) const {
-        float inv = c.l > 0.0f ? 1.0f / c.l : 0.0f;
-        float o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float x = c.a[i] * inv;
-            o[i] = x > 0.0f ? x : expm1f(x);
-        }
-        *reinterpret_cast<uint4 *>(out + (int64_t)v * 64 + lane * 8) = pack8(o);
-    }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
-        float *p = slot + lane * 12;
-        reinterpret_cast<float4 *>(p)[0] = make_float4(c.m, c.l, c.a[0], c.a[1]);
-        reinterpret_cast<float4 *>(p)[1] = make_float4(c.a[2], c.a[3], c.a[4], c.a[5]);
-        reinterpret_cast<float2 *>(p)[4] = make_float2(c.a[6], c.a[7]);
-    }
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
-        const float *p = slot + lane * 12;
-        float4 x = __ldcg(reinterpret_cast<const float4 *>(p));
-        float4 y = __ldcg(reinterpret_cast<const float4 *>(p) + 1);
-        float2 w = __ldcg(reinterpret_cast<const float2 *>(p) + 4);
-        float pm = x.x, pl = x.y;
-        float pa[8] = {x.z, x.w, y.x, y.y, y.z, y.w, w.x, w.y};
-        float mn = fmaxf(c.m, pm);
+    // merge another partial (pm, pl, pa) into c (flash-decoding merge)
+    __device__ __forceinline__ static void merge_parts(Acc &c, float pm, float pl, const float (&pa)[8]) {
+        const float mn = fmaxf(c.m, pm);
         if (mn == -INFINITY) return;  // both empty
-        float co = __expf(c.m - mn), cp = __expf(pm - mn);
+        const float co = __expf(c.m - mn), cp = __expf(pm - mn);
         c.l = c.l * co + pl * cp;
 #pragma unroll
         for (int i = 0; i < 8; ++i) c.a[i] = c.a[i] * co + pa[i] * cp;
         c.m = mn;
     }
+    __device__ __forceinline__ void reduce_xor(Acc &c, int o) const {
+        const float pm = __shfl_xor_sync(kFull, c.m, o), pl = __shfl_xor_sync(kFull, c.l, o);
+        float pa[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pa[i] = __shfl_xor_sync(kFull, c.a[i], o);
+        merge_parts(c, pm, pl, pa);
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int gl, bool store) const {
+        const float inv = c.l > 0.0f ? 1.0f / c.l : 0.0f;
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float x = c.a[i] * inv;
+            o[i] = x > 0.0f ? x : expm1f(x);
+        }
+        if (store) *reinterpret_cast<uint4 *>(out + (int64_t)v * 64 + gl * 8) = pack8(o);
+    }
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int gl) const {
+        float *p = slot + gl * 12;
+        reinterpret_cast<float4 *>(p)[0] = make_float4(c.m, c.l, c.a[0], c.a[1]);
+        reinterpret_cast<float4 *>(p)[1] = make_float4(c.a[2], c.a[3], c.a[4], c.a[5]);
+        reinterpret_cast<float2 *>(p)[4] = make_float2(c.a[6], c.a[7]);
+    }
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int gl) const {
+        const float *p = slot + gl * 12;
+        const float4 x = __ldcg(reinterpret_cast<const float4 *>(p));
+        const float4 y = __ldcg(reinterpret_cast<const float4 *>(p) + 1);
+        const float2 w = __ldcg(reinterpret_cast<const float2 *>(p) + 4);
+        const float pa[8] = {x.z, x.w, y.x, y.y, y.z, y.w, w.x, w.y};
+        merge_parts(c, x.x, x.y, pa);
+    }
 };
 
 // C4: per-edge-type sums of fp32 rows (4 floats per lane, 4 type slots).
 struct TypedF32Op {
-    __device__ void set_smem(const float *) {}
-    static constexpr int kAccF = 16;
+    static constexpr int kWin = 0;
     struct Acc { float a[4][4]; };
     struct Val { float4 x; };
     const float *H;
     int32_t f;
     float *S;  // [n][4][f]
-    __device__ void setup(int) {}
+    __device__ __forceinline__ float row_value(int32_t, int) const { return 0.0f; }
     __device__ __forceinline__ void zero(Acc &c) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
             for (int i = 0; i < 4; ++i) c.a[t][i] = 0.0f;
     }
-    __device__ __forceinline__ void begin_row(int32_t, int) {}
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        return Val{__ldg(reinterpret_cast<const float4 *>(H + (int64_t)u * f) + lane)};
+    __device__ __forceinline__ Val load(int32_t u, int gl) const {
+        return Val{__ldg(reinterpret_cast<const float4 *>(H + (int64_t)u * f) + gl)};
     }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, int32_t t) const {
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t t) const {
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt)
             if (t == tt) {
@@ -302,151 +304,385 @@ struct TypedF32Op {
                 c.a[tt][3] += v.x.w;
             }
     }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, int lane) const {
+    __device__ __forceinline__ void reduce_xor(Acc &c, int o) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            reinterpret_cast<float4 *>(S + ((int64_t)v * 4 + t) * f)[lane] =
+#pragma unroll
+            for (int i = 0; i < 4; ++i) c.a[t][i] += __shfl_xor_sync(kFull, c.a[t][i], o);
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int gl, bool store) const {
+        if (!store) return;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            reinterpret_cast<float4 *>(S + ((int64_t)v * 4 + t) * f)[gl] =
                 make_float4(c.a[t][0], c.a[t][1], c.a[t][2], c.a[t][3]);
     }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int gl) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            reinterpret_cast<float4 *>(slot + t * 128)[lane] = make_float4(c.a[t][0], c.a[t][1], c.a[t][2], c.a[t][3]);
+            reinterpret_cast<float4 *>(slot + t * 128)[gl] = make_float4(c.a[t][0], c.a[t][1], c.a[t][2], c.a[t][3]);
     }
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int gl) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            float4 x = __ldcg(reinterpret_cast<const float4 *>(slot + t * 128) + lane);
+            const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot + t * 128) + gl);
             c.a[t][0] += x.x; c.a[t][1] += x.y; c.a[t][2] += x.z; c.a[t][3] += x.w;
         }
     }
 };
 
-// Ops whose flush needs the whole group (the fused GEMV) implement finish_g.
-template <typename Op, int G>
-__device__ __forceinline__ auto do_finish(Op &op, int32_t v, const typename Op::Acc &c, const Group<G> &grp, int)
-    -> decltype(op.template finish_g<G>(v, c, grp), void()) {
-    op.template finish_g<G>(v, c, grp);
+// Ops whose epilogue needs the whole warp (the fused GEMV) implement finish_w.
+template <typename Op>
+__device__ __forceinline__ auto do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int gl,
+                                          int lane, bool store, const float *Ws, int)
+    -> decltype(op.finish_w(v, c, rs, Ws, lane), void()) {
+    op.finish_w(v, c, rs, Ws, lane);
 }
-template <typename Op, int G>
-__device__ __forceinline__ void do_finish(Op &op, int32_t v, const typename Op::Acc &c, const Group<G> &grp, long) {
-    op.finish(v, c, grp.lane);
+template <typename Op>
+__device__ __forceinline__ void do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int gl, int,
+                                          bool store, const float *, long) {
+    op.finish(v, c, rs, gl, store);
 }
 
-// Contribute the partial `acc` of split row r (edges [rb, re)) to `slot`; the
-// last of its parts (atomic ticket on the task that holds r's end item)
-// merges all parts in task order and writes the row.  Rare path: outlined.
-template <int G, typename Op>
-__device__ __noinline__ void contribute(Op &op, const typename Op::Acc &acc, const Group<G> &grp, AggWorkspace ws,
-                                        int32_t slot_floats, int64_t T, int32_t r, int64_t rb, int64_t re,
-                                        int64_t slot) {
+template <typename Op>
+__device__ __forceinline__ float row_rs(const Op &op, int32_t v, int gl) {
+    return Op::kWin ? op.row_value(v, Op::kWin == 1 ? 0 : gl % (Op::kWin ? Op::kWin : 1)) : 0.0f;
+}
+
+// Split rows (hubs, rows straddling a task boundary): every task holding part
+// of row r saves its fp32 partial (combined over sub-groups) to its slot, then
+// takes an integer ticket on the task k2 that holds r's end item; the last
+// arrival merges all parts in task order and runs the epilogue.  The ticket is
+// taken after the task's main loop (never inside it), so the hot loop carries
+// no call.
+template <typename Op>
+__device__ __forceinline__ void save_partial(const Op &op, const typename Op::Acc &acc, AggWorkspace ws,
+                                             int32_t slot_floats, int64_t slot, int gl, int sub) {
+    if (sub == 0) op.save(ws.partials + slot * slot_floats, acc, gl);
+}
+template <typename Op>
+__device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int32_t slot_floats, int64_t T, int32_t r,
+                                          int64_t rb, int64_t re, int gl, int sub, const float *Ws) {
+    const int lane = threadIdx.x & 31;
     const int64_t k1 = (rb + r) / T, k2 = (re + r) / T;
-    op.save(ws.partials + slot * slot_floats, acc, grp.lane);
     __threadfence();
-    grp.sync();
+    __syncwarp();
     int old = 0;
-    if (grp.lane == 0) old = atomicAdd(ws.counters + k2, 1);
-    old = grp.shfl(old, 0);
+    if (lane == 0) old = atomicAdd(ws.counters + k2, 1);
+    old = __shfl_sync(kFull, old, 0);
     if (old == (int)(k2 - k1)) {
         __threadfence();
         typename Op::Acc m;
         op.zero(m);
-        op.begin_row(r, grp.lane);
-        op.merge(m, ws.partials + (2 * k1 + 1) * slot_floats, grp.lane);
-        for (int64_t kk = k1 + 1; kk <= k2; ++kk) op.merge(m, ws.partials + (2 * kk) * slot_floats, grp.lane);
-        do_finish(op, r, m, grp, 0);
+        op.merge(m, ws.partials + (2 * k1 + 1) * slot_floats, gl);
+        for (int64_t kk = k1 + 1; kk <= k2; ++kk) op.merge(m, ws.partials + (2 * kk) * slot_floats, gl);
+        do_finish(op, r, m, row_rs(op, r, gl), gl, lane, sub == 0, Ws, 0);
     }
 }
 
 // ================================================================== engine ==
-template <int G, int U, bool kTyped, typename Op>
-__global__ void __launch_bounds__(kBlock, 2) k_segreduce(GraphView g, Op op, AggWorkspace ws, int32_t slot_floats,
-                                                      const float *Wg, int32_t w_elems) {
+template <int G, int U, int kMinB, bool kTyped, typename Op>
+__global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, const Op op, const AggWorkspace ws,
+                                                          const int32_t slot_floats, const float *Wg,
+                                                          const int32_t w_elems) {
+    constexpr int S = 32 / G;  // sub-groups (edges per step)
+    constexpr int B = U * S;   // edges per batch
+    static_assert(B <= 32, "a batch must fit in one col_src chunk");
+    constexpr int kWin = Op::kWin;
+    constexpr int kWinD = kWin ? kWin : 1;
+    constexpr int kWinRows = 32 / kWinD;
+
     extern __shared__ float smem_w[];
     if (Wg) {  // stage the ApplyVertex weight (fused-GEMV ops)
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) smem_w[i] = Wg[i];
         __syncthreads();
     }
-    op.set_smem(smem_w);
-    const Group<G> grp;
-    const int64_t k = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / G, gl = lane & (G - 1);
+    const int64_t k = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (k >= g.ntasks) return;
-    op.setup(grp.lane);
 
     const int64_t T = g.T;
+    const int32_t n = g.n;
     int32_t v = g.task_v[k];
-    int64_t p = g.task_p[k];
+    const int32_t p = (int32_t)g.task_p[k];
     const int32_t v1 = g.task_v[k + 1];
-    const int64_t p1 = g.task_p[k + 1];
+    const int32_t p1 = (int32_t)g.task_p[k + 1];
     const int32_t v0 = v;
-    int64_t row_beg = g.row_ptr[v];
-    int64_t row_end = g.row_ptr[v + 1];
+    int32_t row_beg = (int32_t)g.row_ptr[v];
     const bool head = row_beg < p;  // first row began in an earlier task
+    const int32_t head_beg = row_beg;
+    int32_t head_end = -1;          // set when the head row's partial is saved
+
+    // row windows: lane i holds row_end(wr + i); lane i holds value i % kWin
+    // of row wv + i / kWin
+    auto load_re = [&](int32_t wbase) -> int32_t {
+        const int32_t r = wbase + lane;
+        return r < n ? (int32_t)__ldg(g.row_ptr + r + 1) : g.e;
+    };
+    auto load_rv = [&](int32_t wbase) -> float {
+        if (!kWin) return 0.0f;
+        const int32_t r = wbase + lane / kWinD;
+        return r < n ? op.row_value(r, lane % kWinD) : 0.0f;
+    };
+    int32_t wr = v, wv = v;
+    int32_t w_re = load_re(wr);
+    float w_rv = load_rv(wv);
+    int32_t row_end = __shfl_sync(kFull, w_re, 0);
+    float rs = kWin ? __shfl_sync(kFull, w_rv, kWin == 1 ? 0 : gl % kWinD) : 0.0f;
 
     typename Op::Acc acc;
     op.zero(acc);
-    op.begin_row(v, grp.lane);
 
     auto flush = [&]() {
-        if (head && v == v0)
-            contribute<G>(op, acc, grp, ws, slot_floats, T, v, row_beg, row_end, 2 * k);
-        else
-            do_finish(op, v, acc, grp, 0);
+#pragma unroll
+        for (int o = G; o < 32; o <<= 1) op.reduce_xor(acc, o);
+        if (head && v == v0) {
+            save_partial(op, acc, ws, slot_floats, 2 * k, gl, sub);
+            head_end = row_end;
+        } else {
+            do_finish(op, v, acc, rs, gl, lane, sub == 0, smem_w, 0);
+        }
         ++v;
         row_beg = row_end;
-        if (v < g.n) row_end = g.row_ptr[v + 1];
+        if (v - wr == 32) {
+            wr += 32;
+            w_re = load_re(wr);
+        }
+        row_end = __shfl_sync(kFull, w_re, v - wr);
+        if (kWin) {
+            if (v - wv == kWinRows) {
+                wv += kWinRows;
+                w_rv = load_rv(wv);
+            }
+            rs = __shfl_sync(kFull, w_rv, (v - wv) * kWinD + (kWin == 1 ? 0 : gl % kWinD));
+        }
         op.zero(acc);
-        if (v < g.n) op.begin_row(v, grp.lane);
     };
 
-    for (int64_t q0 = p; q0 < p1; q0 += G) {
-        const int cnt = (int)(p1 - q0 < (int64_t)G ? p1 - q0 : (int64_t)G);
-        const int32_t cs = grp.lane < cnt ? __ldg(g.col_src + q0 + grp.lane) : 0;
-        int32_t ct = 0;
-        if (kTyped) ct = grp.lane < cnt ? __ldg(g.etype + q0 + grp.lane) : 0;
-        for (int j0 = 0; j0 < cnt; j0 += U) {
-            // issue U independent row gathers, then consume them row segment by
-            // row segment (one copy of the flush code per batch)
-            typename Op::Val vals[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int32_t src = grp.shfl(cs, (j0 + u) & (G - 1));
-                if (j0 + u < cnt) vals[u] = op.load(src, grp.lane);
-            }
-            const int nb = cnt - j0 < U ? cnt - j0 : U;
-            const int64_t qb = q0 + j0;
-            int u0 = 0;
-            while (true) {
-                const int64_t lim64 = row_end - qb;
-                const int lim = lim64 < (int64_t)nb ? (int)lim64 : nb;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    int32_t t = 0;
-                    if (kTyped) t = grp.shfl(ct, (j0 + u) & (G - 1));
-                    if (u >= u0 && u < lim) op.add(acc, vals[u], t);
-                }
-                if (lim >= nb) break;
-                u0 = lim;
-                do flush(); while (qb + u0 >= row_end);
-            }
+    // col_src / etype in 32-edge chunks, one chunk ahead
+    auto load_cs = [&](int32_t base) -> int32_t {
+        const int32_t q = base + lane;
+        return q < p1 ? __ldcs(g.col_src + q) : 0;
+    };
+    auto load_ct = [&](int32_t base) -> int32_t {
+        const int32_t q = base + lane;
+        return (kTyped && q < p1) ? __ldcs(g.etype + q) : 0;
+    };
+    int32_t cb = p;
+    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32);
+    int32_t ct_a = load_ct(cb), ct_b = load_ct(cb + 32);
+
+    int32_t q = p;
+    while (true) {
+        while (v < v1 && row_end <= q) flush();  // rows whose edges are all consumed
+        if (q >= p1) break;
+        const int32_t lim = row_end < p1 ? row_end : p1;
+        const int c = lim - q < B ? (int)(lim - q) : B;
+        if (q - cb >= 32) {
+            cb += 32;
+            cs_a = cs_b;
+            ct_a = ct_b;
+            cs_b = load_cs(cb + 32);
+            ct_b = load_ct(cb + 32);
         }
+        const int base = q - cb;
+        typename Op::Val val[U];
+        int32_t ty[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+            const int e = t * S + sub;
+            const int idx = base + e;
+            const int32_t sa = __shfl_sync(kFull, cs_a, idx & 31);
+            const int32_t sb = __shfl_sync(kFull, cs_b, idx & 31);
+            if (kTyped) {
+                const int32_t ta = __shfl_sync(kFull, ct_a, idx & 31);
+                const int32_t tb = __shfl_sync(kFull, ct_b, idx & 31);
+                ty[t] = idx < 32 ? ta : tb;
+            } else {
+                ty[t] = 0;
+            }
+            if (e < c) val[t] = op.load(idx < 32 ? sa : sb, gl);
+        }
+#pragma unroll
+        for (int t = 0; t < U; ++t)
+            if (t * S + sub < c) op.add(acc, val[t], rs, ty[t]);
+        q += c;
     }
-    while (v < v1) flush();
-    if (v < g.n && p1 > row_beg) {  // tail: row v continues into the next task
+    if (v < n && p1 > row_beg) {  // tail: row v continues into the next task
+#pragma unroll
+        for (int o = G; o < 32; o <<= 1) op.reduce_xor(acc, o);
         const int64_t slot = (head && v == v0) ? 2 * k : 2 * k + 1;
-        contribute<G>(op, acc, grp, ws, slot_floats, T, v, row_beg, row_end, slot);
+        save_partial(op, acc, ws, slot_floats, slot, gl, sub);
+        ticket_merge(op, ws, slot_floats, T, v, row_beg, row_end, gl, sub, smem_w);
     }
+    if (head_end >= 0 && !(v == v0))  // head row ended inside this task
+        ticket_merge(op, ws, slot_floats, T, v0, head_beg, head_end, gl, sub, smem_w);
 }
 
-template <int G, int U, bool kTyped, typename Op>
+// Dense variant for full-warp rows (G = 32: one edge per step): batches are
+// U CONSECUTIVE edges of the task regardless of row ends, so every batch
+// keeps U row gathers in flight; the adds are unpredicated and a row end is
+// a warp-uniform test after each edge (taken once per row).
+template <int U, int kMinB, bool kTyped, typename Op>
+__global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphView g, const Op op,
+                                                                const AggWorkspace ws, const int32_t slot_floats) {
+    constexpr int kWin = Op::kWin;
+    static_assert(kWin <= 1, "dense engine supports per-row scalars only");
+    const int lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (k >= g.ntasks) return;
+
+    const int64_t T = g.T;
+    const int32_t n = g.n;
+    int32_t v = g.task_v[k];
+    const int32_t p = (int32_t)g.task_p[k];
+    const int32_t v1 = g.task_v[k + 1];
+    const int32_t p1 = (int32_t)g.task_p[k + 1];
+    const int32_t v0 = v;
+    int32_t row_beg = (int32_t)g.row_ptr[v];
+    const bool head = row_beg < p;
+    const int32_t head_beg = row_beg;
+    int32_t head_end = -1;
+
+    int32_t wr = v;
+    int32_t w_re = (wr + lane < n) ? (int32_t)__ldg(g.row_ptr + wr + lane + 1) : g.e;
+    float w_rv = (kWin && wr + lane < n) ? op.row_value(wr + lane, 0) : 0.0f;
+    int32_t row_end = __shfl_sync(kFull, w_re, 0);
+    float rs = kWin ? __shfl_sync(kFull, w_rv, 0) : 0.0f;
+
+    typename Op::Acc acc;
+    op.zero(acc);
+
+    auto flush = [&]() {
+        if (head && v == v0) {
+            save_partial(op, acc, ws, slot_floats, 2 * k, lane, 0);
+            head_end = row_end;
+        } else {
+            op.finish(v, acc, rs, lane, true);
+        }
+        ++v;
+        row_beg = row_end;
+        if (v - wr == 32) {
+            wr += 32;
+            w_re = (wr + lane < n) ? (int32_t)__ldg(g.row_ptr + wr + lane + 1) : g.e;
+            if (kWin) w_rv = (wr + lane < n) ? op.row_value(wr + lane, 0) : 0.0f;
+        }
+        row_end = __shfl_sync(kFull, w_re, v - wr);
+        if (kWin) rs = __shfl_sync(kFull, w_rv, v - wr);
+        op.zero(acc);
+    };
+
+    auto load_cs = [&](int32_t base) -> int32_t {
+        const int32_t q = base + lane;
+        return q < p1 ? __ldcs(g.col_src + q) : 0;
+    };
+    auto load_ct = [&](int32_t base) -> int32_t {
+        const int32_t q = base + lane;
+        return (kTyped && q < p1) ? __ldcs(g.etype + q) : 0;
+    };
+    int32_t cb = p;
+    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32);
+    int32_t ct_a = load_ct(cb), ct_b = load_ct(cb + 32);
+    auto slide = [&](int32_t q) {
+        if (q - cb >= 32) {
+            cb += 32;
+            cs_a = cs_b;
+            ct_a = ct_b;
+            cs_b = load_cs(cb + 32);
+            ct_b = load_ct(cb + 32);
+        }
+    };
+
+    while (v < v1 && row_end <= p) flush();  // rows that end before the first edge
+    int32_t q = p;
+    for (; q + U <= p1; q += U) {
+        slide(q);
+        const int base = q - cb;
+        typename Op::Val val[U];
+        int32_t ty[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = base + u;
+            const int32_t sa = __shfl_sync(kFull, cs_a, idx & 31);
+            const int32_t sb = __shfl_sync(kFull, cs_b, idx & 31);
+            ty[u] = 0;
+            if (kTyped) {
+                const int32_t ta = __shfl_sync(kFull, ct_a, idx & 31);
+                const int32_t tb = __shfl_sync(kFull, ct_b, idx & 31);
+                ty[u] = idx < 32 ? ta : tb;
+            }
+            val[u] = op.load(idx < 32 ? sa : sb, lane);
+        }
+        if (row_end >= q + U) {
+            // fast path: no row ends strictly inside the batch
+#pragma unroll
+            for (int u = 0; u < U; ++u) op.add(acc, val[u], rs, ty[u]);
+        } else {
+            // slow path: reduce segment by segment, one flush site
+            int u0 = 0;
+            while (true) {
+                const int lim = row_end - q < U ? (int)(row_end - q) : U;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (u >= u0 && u < lim) op.add(acc, val[u], rs, ty[u]);
+                if (lim >= U) break;
+                u0 = lim;
+                do flush(); while (v < v1 && row_end <= q + u0);
+            }
+        }
+        while (v < v1 && row_end == q + U) flush();
+    }
+    for (; q < p1; ++q) {  // remainder, one edge at a time
+        slide(q);
+        const int idx = q - cb;
+        const int32_t sa = __shfl_sync(kFull, cs_a, idx & 31);
+        const int32_t sb = __shfl_sync(kFull, cs_b, idx & 31);
+        int32_t t = 0;
+        if (kTyped) {
+            const int32_t ta = __shfl_sync(kFull, ct_a, idx & 31);
+            const int32_t tb = __shfl_sync(kFull, ct_b, idx & 31);
+            t = idx < 32 ? ta : tb;
+        }
+        op.add(acc, op.load(idx < 32 ? sa : sb, lane), rs, t);
+        while (v < v1 && row_end == q + 1) flush();
+    }
+    while (v < v1) flush();
+    if (v < n && p1 > row_beg) {  // tail: row v continues into the next task
+        const int64_t slot = (head && v == v0) ? 2 * k : 2 * k + 1;
+        save_partial(op, acc, ws, slot_floats, slot, lane, 0);
+        ticket_merge(op, ws, slot_floats, T, v, row_beg, row_end, lane, 0, nullptr);
+    }
+    if (head_end >= 0 && !(v == v0))
+        ticket_merge(op, ws, slot_floats, T, v0, head_beg, head_end, lane, 0, nullptr);
+}
+
+template <int U, bool kTyped, int kMinB, typename Op>
+cudaError_t run_dense(const GraphDev &g, const Op &op, AggWorkspace ws, int32_t slot_floats, cudaStream_t st) {
+    if (g.ntasks == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((g.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    k_segreduce_dense<U, kMinB, kTyped, Op><<<blocks, kBlock, 0, st>>>(view(g), op, ws, slot_floats);
+    return cudaGetLastError();
+}
+
+template <int G, int U, bool kTyped, int kMinB, typename Op>
 cudaError_t run(const GraphDev &g, const Op &op, AggWorkspace ws, int32_t slot_floats, cudaStream_t st,
                 const float *Wg = nullptr, int32_t w_elems = 0) {
     if (g.ntasks == 0) return cudaSuccess;
-    const int64_t groups_per_block = kBlock / G;
-    const unsigned blocks = (unsigned)((g.ntasks + groups_per_block - 1) / groups_per_block);
+    const unsigned blocks = (unsigned)((g.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const size_t smem = Wg ? sizeof(float) * w_elems : 0;
-    k_segreduce<G, U, kTyped, Op><<<blocks, kBlock, smem, st>>>(view(g), op, ws, slot_floats, Wg, w_elems);
+    k_segreduce<G, U, kMinB, kTyped, Op><<<blocks, kBlock, smem, st>>>(view(g), op, ws, slot_floats, Wg, w_elems);
     return cudaGetLastError();
+}
+
+// Development knob: SAGA_AGG_VARIANT selects the (U, blocks/SM) instance of
+// the G = 32 bf16 sum kernel, for measuring the register / in-flight trade-off.
+int agg_variant() {
+    static int v = [] {
+        const char *s = getenv("SAGA_AGG_VARIANT");
+        return s ? atoi(s) : 0;
+    }();
+    return v;
 }
 
 }  // namespace
@@ -461,42 +697,48 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
     return 0;
 }
 
-cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
-                                __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    SumBf16Op op{};
-    op.X = Y; op.f = f; op.scale = g.dinv; op.bias = bias; op.act = act; op.out = out;
+template <int kAct>
+cudaError_t agg_sum_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, const float *scale,
+                         const float *bias, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
+    SumBf16Op<kAct> op{};
+    op.X = X; op.f = f; op.scale = scale; op.bias = bias; op.out = out;
     switch (f) {
-        case 256: return run<32, 8, false>(g, op, ws, f, st);
-        case 128: return run<16, 8, false>(g, op, ws, f, st);
-        case 64: return run<8, 8, false>(g, op, ws, f, st);
+        case 256:
+            switch (agg_variant()) {
+                case 1: return run_dense<8, false, 3>(g, op, ws, f, st);
+                case 2: return run_dense<8, false, 2>(g, op, ws, f, st);
+                case 3: return run_dense<8, false, 4>(g, op, ws, f, st);
+                case 4: return run_dense<6, false, 4>(g, op, ws, f, st);
+                case 5: return run_dense<4, false, 4>(g, op, ws, f, st);
+            }
+            return run_dense<4, false, 4>(g, op, ws, f, st);
+        case 128: return run<16, 8, false, 3>(g, op, ws, f, st);
+        case 64: return run<8, 4, false, 3>(g, op, ws, f, st);
     }
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
+                                __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
+    if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(g, Y, f, g.dinv, bias, out, ws, st);
+    return agg_sum_bf16<SAGA_ACT_NONE>(g, Y, f, g.dinv, bias, out, ws, st);
+}
+
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
                                  AggWorkspace ws, cudaStream_t st) {
-    SumBf16Op op{};
-    op.X = X; op.f = f; op.scale = g.inv_deg; op.bias = nullptr; op.act = SAGA_ACT_NONE; op.out = M;
-    switch (f) {
-        case 256: return run<32, 8, false>(g, op, ws, f, st);
-        case 128: return run<16, 8, false>(g, op, ws, f, st);
-        case 64: return run<8, 8, false>(g, op, ws, f, st);
-    }
-    return cudaErrorInvalidValue;
+    return agg_sum_bf16<SAGA_ACT_NONE>(g, X, f, g.inv_deg, nullptr, M, ws, st);
 }
 
 cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                                  const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st) {
     GcnF32FusedOp op{};
-    op.X = X; op.f_in = f_in; op.f_out = f_out; op.dinv = g.dinv; op.W = W; op.bias = bias; op.act = act;
-    op.out = out;
-    op.Ws = nullptr;  // set on device to the dynamic shared array
+    op.X = X; op.f_in = f_in; op.f_out = f_out; op.dinv = g.dinv; op.bias = bias; op.act = act; op.out = out;
     const int32_t welems = f_in * f_out;
     switch (f_in) {
-        case 128: return run<32, 4, false>(g, op, ws, f_in, st, W, welems);
-        case 64: return run<16, 4, false>(g, op, ws, f_in, st, W, welems);
-        case 32: return run<8, 4, false>(g, op, ws, f_in, st, W, welems);
-        case 16: return run<4, 4, false>(g, op, ws, f_in, st, W, welems);
+        case 128: return run<32, 4, false, 2>(g, op, ws, f_in, st, W, welems);
+        case 64: return run<16, 4, false, 2>(g, op, ws, f_in, st, W, welems);
+        case 32: return run<8, 4, false, 2>(g, op, ws, f_in, st, W, welems);
+        case 16: return run<4, 4, false, 2>(g, op, ws, f_in, st, W, welems);
     }
     return cudaErrorInvalidValue;
 }
@@ -505,7 +747,7 @@ cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const flo
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
     GatOp op{};
     op.z = z; op.el = el; op.er = er; op.slope = slope; op.out = out;
-    return run<8, 8, false>(g, op, ws, 8 * 12, st);
+    return run<8, 4, false, 3>(g, op, ws, 8 * 12, st);
 }
 
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, AggWorkspace ws,
@@ -513,8 +755,8 @@ cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, f
     TypedF32Op op{};
     op.H = H; op.f = f; op.S = S;
     if (f != 128) return cudaErrorInvalidValue;
-    if (g.etype) return run<32, 8, true>(g, op, ws, 4 * f, st);
-    return run<32, 8, false>(g, op, ws, 4 * f, st);
+    if (g.etype) return run_dense<8, true, 2>(g, op, ws, 4 * f, st);
+    return run_dense<8, false, 2>(g, op, ws, 4 * f, st);
 }
 
 }  // namespace saga

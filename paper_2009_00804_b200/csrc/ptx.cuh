@@ -187,6 +187,23 @@ __device__ __forceinline__ uint4 ldg_nc_v4_policy(const void *p, uint64_t policy
                  : "l"(p), "l"(policy));
     return r;
 }
+// Feature-row gather load.  mode 0: L1 no-allocate (L2 treats it as
+// evict-first); 1: plain non-coherent (L2 evict-normal); 2: L1 no-allocate
+// with an explicit L2 cache-policy register.
+__device__ __forceinline__ uint4 ldg_row_v4(const void *p, int mode, uint64_t policy) {
+    uint4 r;
+    if (mode == 1)
+        asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (mode == 2)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p), "l"(policy));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -194,13 +211,22 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
                  : "l"(p));
     return r;
 }
-// Streaming 16-byte store (evict-first in L2).
+// Streaming 16-byte store (L2 evict-first cache policy).
 __device__ __forceinline__ void stg_v4_stream(void *p, uint4 v) {
-    asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
+    asm volatile(
+        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, pol;\n}" ::"l"(p),
+        "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+        : "memory");
 }
 
+// acc[0..1] += the two bf16 halves of `u`, in fp32 (sm_100 mixed-precision
+// add: one FHADD.BF16 per element, no unpacking).
+__device__ __forceinline__ void add_bf16x2_f32(float &lo, float &hi, uint32_t u) {
+    asm("{\n.reg .b16 l, h;\nmov.b32 {l, h}, %2;\nadd.rn.f32.bf16 %0, l, %0;\nadd.rn.f32.bf16 %1, h, %1;\n}"
+        : "+f"(lo), "+f"(hi)
+        : "r"(u));
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&h);
