@@ -96,10 +96,23 @@ struct SumBf16Op {
 #pragma unroll
         for (int i = 0; i < 8; ++i) c.a[i] = 0.0f;
     }
+    // row u, lane gl: one IMAD.WIDE.U32 per address (row byte offsets < 2^32
+    // is guaranteed by saga_layer's size checks)
     __device__ __forceinline__ Val load(int32_t u, int gl) const {
-        return Val{__ldg(reinterpret_cast<const uint4 *>(X + (int64_t)u * f) + gl)};
+        const char *base = reinterpret_cast<const char *>(X) + gl * 16;
+        return Val{__ldg(reinterpret_cast<const uint4 *>(base + (uint64_t)(uint32_t)u * (uint32_t)(f * 2)))};
     }
+    int unpack;
     __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t) const {
+        if (unpack) {
+            const uint32_t q[4] = {v.x.x, v.x.y, v.x.z, v.x.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                c.a[2 * i] += __uint_as_float(q[i] << 16);
+                c.a[2 * i + 1] += __uint_as_float(q[i] & 0xffff0000u);
+            }
+            return;
+        }
         ptx::add_bf16x2_f32(c.a[0], c.a[1], v.x.x);
         ptx::add_bf16x2_f32(c.a[2], c.a[3], v.x.y);
         ptx::add_bf16x2_f32(c.a[4], c.a[5], v.x.z);
@@ -109,18 +122,19 @@ struct SumBf16Op {
 #pragma unroll
         for (int i = 0; i < 8; ++i) c.a[i] += __shfl_xor_sync(kFull, c.a[i], o);
     }
+    // epilogue in two 4-wide halves (keeps the flush's register peak low)
     __device__ __forceinline__ void finish(int32_t v, const Acc &c, float rs, int gl, bool store) const {
-        float b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (bias) {
-            const float4 *bp = reinterpret_cast<const float4 *>(bias + gl * 8);
-            const float4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
-            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-            b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-        }
-        float o[8];
+        uint32_t pk[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = act_fn(fmaf(rs, c.a[i], b[i]), kAct);
-        if (store) *reinterpret_cast<uint4 *>(out + (int64_t)v * f + gl * 8) = pack8(o);
+        for (int h = 0; h < 2; ++h) {
+            float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bias) b = __ldg(reinterpret_cast<const float4 *>(bias + gl * 8) + h);
+            pk[2 * h] = ptx::pack_bf16x2(act_fn(fmaf(rs, c.a[4 * h + 0], b.x), kAct),
+                                         act_fn(fmaf(rs, c.a[4 * h + 1], b.y), kAct));
+            pk[2 * h + 1] = ptx::pack_bf16x2(act_fn(fmaf(rs, c.a[4 * h + 2], b.z), kAct),
+                                             act_fn(fmaf(rs, c.a[4 * h + 3], b.w), kAct));
+        }
+        if (store) *reinterpret_cast<uint4 *>(out + (int64_t)v * f + gl * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int gl) const {
         float4 *p = reinterpret_cast<float4 *>(slot + gl * 8);
@@ -292,7 +306,8 @@ struct TypedF32Op {
             for (int i = 0; i < 4; ++i) c.a[t][i] = 0.0f;
     }
     __device__ __forceinline__ Val load(int32_t u, int gl) const {
-        return Val{__ldg(reinterpret_cast<const float4 *>(H + (int64_t)u * f) + gl)};
+        const char *base = reinterpret_cast<const char *>(H) + gl * 16;
+        return Val{__ldg(reinterpret_cast<const float4 *>(base + (uint64_t)(uint32_t)u * (uint32_t)(f * 4)))};
     }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t t) const {
 #pragma unroll
@@ -522,54 +537,77 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
 
 // Dense variant for full-warp rows (G = 32: one edge per step): batches are
 // U CONSECUTIVE edges of the task regardless of row ends, so every batch
-// keeps U row gathers in flight; the adds are unpredicated and a row end is
-// a warp-uniform test after each edge (taken once per row).
+// keeps U row gathers in flight and the adds are unpredicated.  A batch in
+// which a row ends takes the slow path: its U rows are parked in a per-warp
+// shared-memory slot (each lane re-reads only what it wrote) and reduced edge
+// by edge with a row-end test after each.  Everything the fast path does not
+// touch (row windows, head bookkeeping) lives in a per-warp shared record, so
+// the registers go to in-flight rows: U = 8 fits 64 registers without spills
+// (32 warps per SM, 256 rows of 512 B in flight per SM).
+template <int U>
+struct DenseWarp {
+    uint4 park[U][32];
+    int32_t re[32];  // row_end of rows wr .. wr+31
+    float rv[32];    // epilogue scalar of the same rows
+    int32_t wr, v0, row_beg, head_beg, head_end, head;
+};
+
 template <int U, int kMinB, bool kTyped, typename Op>
 __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphView g, const Op op,
-                                                                const AggWorkspace ws, const int32_t slot_floats) {
+                                                                const AggWorkspace ws, const int32_t slot_floats,
+                                                                const int dbg) {
     constexpr int kWin = Op::kWin;
     static_assert(kWin <= 1, "dense engine supports per-row scalars only");
+    static_assert(32 % U == 0, "U must divide the 32-edge chunk");
+    static_assert(sizeof(typename Op::Val) == 16, "dense engine parks 16-byte records");
+    __shared__ DenseWarp<U> warps[kWarpsPerBlock];
+    DenseWarp<U> &W = warps[threadIdx.x >> 5];
+    volatile DenseWarp<U> &VW = W;
     const int lane = threadIdx.x & 31;
     const int64_t k = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (k >= g.ntasks) return;
 
-    const int64_t T = g.T;
-    const int32_t n = g.n;
     int32_t v = g.task_v[k];
     const int32_t p = (int32_t)g.task_p[k];
     const int32_t v1 = g.task_v[k + 1];
     const int32_t p1 = (int32_t)g.task_p[k + 1];
-    const int32_t v0 = v;
-    int32_t row_beg = (int32_t)g.row_ptr[v];
-    const bool head = row_beg < p;
-    const int32_t head_beg = row_beg;
-    int32_t head_end = -1;
 
-    int32_t wr = v;
-    int32_t w_re = (wr + lane < n) ? (int32_t)__ldg(g.row_ptr + wr + lane + 1) : g.e;
-    float w_rv = (kWin && wr + lane < n) ? op.row_value(wr + lane, 0) : 0.0f;
-    int32_t row_end = __shfl_sync(kFull, w_re, 0);
-    float rs = kWin ? __shfl_sync(kFull, w_rv, 0) : 0.0f;
+    auto fill_window = [&](int32_t wbase) {
+        const int32_t r = wbase + lane;
+        const bool in = r < g.n;
+        VW.re[lane] = in ? (int32_t)__ldg(g.row_ptr + r + 1) : g.e;
+        VW.rv[lane] = (kWin && in) ? op.row_value(r, 0) : 0.0f;
+        if (lane == 0) VW.wr = wbase;
+        __syncwarp();
+    };
+    if (lane == 0) {
+        const int32_t rb = (int32_t)g.row_ptr[v];
+        VW.v0 = v;
+        VW.row_beg = rb;
+        VW.head_beg = rb;
+        VW.head_end = -1;
+        VW.head = rb < p;
+    }
+    fill_window(v);
+    int32_t row_end = VW.re[0];
 
     typename Op::Acc acc;
     op.zero(acc);
 
+    // finish row v (or save its partial if it is the head row), advance to v+1
     auto flush = [&]() {
-        if (head && v == v0) {
+        const int32_t wr = VW.wr;
+        if (VW.head && v == VW.v0) {
             save_partial(op, acc, ws, slot_floats, 2 * k, lane, 0);
-            head_end = row_end;
+            if (lane == 0) VW.head_end = row_end;
         } else {
-            op.finish(v, acc, rs, lane, true);
+            op.finish(v, acc, VW.rv[v - wr], lane, !(dbg & 1));
         }
         ++v;
-        row_beg = row_end;
-        if (v - wr == 32) {
-            wr += 32;
-            w_re = (wr + lane < n) ? (int32_t)__ldg(g.row_ptr + wr + lane + 1) : g.e;
-            if (kWin) w_rv = (wr + lane < n) ? op.row_value(wr + lane, 0) : 0.0f;
-        }
-        row_end = __shfl_sync(kFull, w_re, v - wr);
-        if (kWin) rs = __shfl_sync(kFull, w_rv, v - wr);
+        __syncwarp();
+        if (lane == 0) VW.row_beg = row_end;
+        if (v - wr == 32) fill_window(wr + 32);
+        row_end = VW.re[v - VW.wr];
         op.zero(acc);
     };
 
@@ -584,6 +622,8 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
     int32_t cb = p;
     int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32);
     int32_t ct_a = load_ct(cb), ct_b = load_ct(cb + 32);
+    // keeps q - cb < 32; batches start at p + multiple of U and U | 32, so a
+    // batch never straddles a chunk
     auto slide = [&](int32_t q) {
         if (q - cb >= 32) {
             cb += 32;
@@ -600,68 +640,58 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
         slide(q);
         const int base = q - cb;
         typename Op::Val val[U];
-        int32_t ty[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int idx = base + u;
-            const int32_t sa = __shfl_sync(kFull, cs_a, idx & 31);
-            const int32_t sb = __shfl_sync(kFull, cs_b, idx & 31);
-            ty[u] = 0;
-            if (kTyped) {
-                const int32_t ta = __shfl_sync(kFull, ct_a, idx & 31);
-                const int32_t tb = __shfl_sync(kFull, ct_b, idx & 31);
-                ty[u] = idx < 32 ? ta : tb;
-            }
-            val[u] = op.load(idx < 32 ? sa : sb, lane);
-        }
-        if (row_end >= q + U) {
-            // fast path: no row ends strictly inside the batch
+        for (int u = 0; u < U; ++u) val[u] = op.load(__shfl_sync(kFull, cs_a, base + u), lane);
+        if ((dbg & 2) || row_end > q + U) {
+            // fast path: no row ends inside the batch
 #pragma unroll
-            for (int u = 0; u < U; ++u) op.add(acc, val[u], rs, ty[u]);
+            for (int u = 0; u < U; ++u) op.add(acc, val[u], 0.0f, kTyped ? __shfl_sync(kFull, ct_a, base + u) : 0);
         } else {
-            // slow path: reduce segment by segment, one flush site
-            int u0 = 0;
-            while (true) {
-                const int lim = row_end - q < U ? (int)(row_end - q) : U;
+            // slow path: park the batch, reduce edge by edge
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (u >= u0 && u < lim) op.add(acc, val[u], rs, ty[u]);
-                if (lim >= U) break;
-                u0 = lim;
-                do flush(); while (v < v1 && row_end <= q + u0);
+            for (int u = 0; u < U; ++u) W.park[u][lane] = *reinterpret_cast<const uint4 *>(&val[u]);
+#pragma unroll 1
+            for (int u = 0; u < U; ++u) {
+                const int32_t t = kTyped ? __shfl_sync(kFull, ct_a, base + u) : 0;
+                const uint4 x = W.park[u][lane];
+                op.add(acc, *reinterpret_cast<const typename Op::Val *>(&x), 0.0f, t);
+                while (v < v1 && row_end == q + u + 1) flush();
             }
         }
-        while (v < v1 && row_end == q + U) flush();
     }
     for (; q < p1; ++q) {  // remainder, one edge at a time
         slide(q);
         const int idx = q - cb;
-        const int32_t sa = __shfl_sync(kFull, cs_a, idx & 31);
-        const int32_t sb = __shfl_sync(kFull, cs_b, idx & 31);
-        int32_t t = 0;
-        if (kTyped) {
-            const int32_t ta = __shfl_sync(kFull, ct_a, idx & 31);
-            const int32_t tb = __shfl_sync(kFull, ct_b, idx & 31);
-            t = idx < 32 ? ta : tb;
-        }
-        op.add(acc, op.load(idx < 32 ? sa : sb, lane), rs, t);
+        const int32_t t = kTyped ? __shfl_sync(kFull, ct_a, idx) : 0;
+        op.add(acc, op.load(__shfl_sync(kFull, cs_a, idx), lane), 0.0f, t);
         while (v < v1 && row_end == q + 1) flush();
     }
+    if (dbg & 2) return;
     while (v < v1) flush();
-    if (v < n && p1 > row_beg) {  // tail: row v continues into the next task
-        const int64_t slot = (head && v == v0) ? 2 * k : 2 * k + 1;
-        save_partial(op, acc, ws, slot_floats, slot, lane, 0);
-        ticket_merge(op, ws, slot_floats, T, v, row_beg, row_end, lane, 0, nullptr);
+    const int32_t v0 = VW.v0, row_beg = VW.row_beg;
+    const bool head = VW.head;
+    if (v < g.n && p1 > row_beg) {  // tail: row v continues into the next task
+        const int64_t sl = (head && v == v0) ? 2 * k : 2 * k + 1;
+        save_partial(op, acc, ws, slot_floats, sl, lane, 0);
+        ticket_merge(op, ws, slot_floats, g.T, v, row_beg, row_end, lane, 0, nullptr);
     }
-    if (head_end >= 0 && !(v == v0))
-        ticket_merge(op, ws, slot_floats, T, v0, head_beg, head_end, lane, 0, nullptr);
+    const int32_t head_end = VW.head_end;
+    if (head_end >= 0 && v != v0)  // the head row ended inside this task
+        ticket_merge(op, ws, slot_floats, g.T, v0, VW.head_beg, head_end, lane, 0, nullptr);
 }
 
+int agg_dbg() {
+    static int v = [] {
+        const char *s = getenv("SAGA_AGG_DBG");
+        return s ? atoi(s) : 0;
+    }();
+    return v;
+}
 template <int U, bool kTyped, int kMinB, typename Op>
 cudaError_t run_dense(const GraphDev &g, const Op &op, AggWorkspace ws, int32_t slot_floats, cudaStream_t st) {
     if (g.ntasks == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((g.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    k_segreduce_dense<U, kMinB, kTyped, Op><<<blocks, kBlock, 0, st>>>(view(g), op, ws, slot_floats);
+    k_segreduce_dense<U, kMinB, kTyped, Op><<<blocks, kBlock, 0, st>>>(view(g), op, ws, slot_floats, agg_dbg());
     return cudaGetLastError();
 }
 
@@ -701,17 +731,15 @@ template <int kAct>
 cudaError_t agg_sum_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, const float *scale,
                          const float *bias, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
     SumBf16Op<kAct> op{};
-    op.X = X; op.f = f; op.scale = scale; op.bias = bias; op.out = out;
+    op.X = X; op.f = f; op.scale = scale; op.bias = bias; op.out = out; op.unpack = (agg_dbg() & 4) != 0;
     switch (f) {
         case 256:
             switch (agg_variant()) {
                 case 1: return run_dense<8, false, 3>(g, op, ws, f, st);
-                case 2: return run_dense<8, false, 2>(g, op, ws, f, st);
-                case 3: return run_dense<8, false, 4>(g, op, ws, f, st);
-                case 4: return run_dense<6, false, 4>(g, op, ws, f, st);
-                case 5: return run_dense<4, false, 4>(g, op, ws, f, st);
+                case 2: return run_dense<4, false, 4>(g, op, ws, f, st);
+                case 3: return run_dense<8, false, 2>(g, op, ws, f, st);
             }
-            return run_dense<4, false, 4>(g, op, ws, f, st);
+            return run_dense<8, false, 4>(g, op, ws, f, st);
         case 128: return run<16, 8, false, 3>(g, op, ws, f, st);
         case 64: return run<8, 4, false, 3>(g, op, ws, f, st);
     }

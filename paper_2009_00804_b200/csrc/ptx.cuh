@@ -211,6 +211,11 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
                  : "l"(p));
     return r;
 }
+// Bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2.
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Streaming 16-byte store (L2 evict-first cache policy).
 __device__ __forceinline__ void stg_v4_stream(void *p, uint4 v) {
     asm volatile(
