@@ -84,6 +84,7 @@ __device__ __forceinline__ float act_fn(float x, int act) {
 template <int kAct>
 struct SumBf16Op {
     static constexpr int kWin = 1;
+    __device__ static int win_col(int) { return 0; }
     struct Acc { float a[8]; };
     struct Val { uint4 x; };
     const __nv_bfloat16 *X;
@@ -290,9 +291,67 @@ struct GatOp {
     }
 };
 
+// C3 on the dense engine: all 32 lanes work on ONE edge; lane L owns head
+// h = L / 4 and output columns 2L, 2L+1 (a 4-byte slice of the 128-byte z
+// row).  Per edge s = LeakyReLU(el[u,h] + er[v,h]) (A14) and a single-exp
+// online-softmax update: with d = s - m, e = exp(-|d|); if d > 0 the state is
+// rescaled by e and the new term weighs 1, else the new term weighs e.
+struct GatDenseOp {
+    static constexpr int kWin = 8;
+    __device__ static int win_col(int lane) { return lane >> 2; }
+    struct Acc { float m, l, a0, a1; };
+    struct Val { uint32_t z2; float el; };
+    const __nv_bfloat16 *z;
+    const float *el, *er;
+    float slope;
+    __nv_bfloat16 *out;
+    __device__ __forceinline__ float row_value(int32_t v, int j) const { return __ldg(er + (int64_t)v * 8 + j); }
+    __device__ __forceinline__ void zero(Acc &c) const { c.m = -INFINITY; c.l = 0.f; c.a0 = 0.f; c.a1 = 0.f; }
+    __device__ __forceinline__ Val load(int32_t u, int lane) const {
+        Val v;
+        v.z2 = __ldg(reinterpret_cast<const uint32_t *>(z + (int64_t)u * 64) + lane);
+        v.el = __ldg(el + (int64_t)u * 8 + (lane >> 2));
+        return v;
+    }
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h, int32_t) const {
+        float s = v.el + er_h;
+        s = s > 0.0f ? s : slope * s;
+        const float d = s - c.m;                 // +inf for the first term
+        const float e = __expf(-fabsf(d));       // 0 for the first term
+        const bool up = d > 0.0f;
+        const float co = up ? e : 1.0f, cn = up ? 1.0f : e;
+        const float2 f = ptx::unpack_bf16x2(v.z2);
+        c.l = fmaf(c.l, co, cn);
+        c.a0 = fmaf(c.a0, co, cn * f.x);
+        c.a1 = fmaf(c.a1, co, cn * f.y);
+        c.m = up ? s : c.m;
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, bool store) const {
+        const float inv = c.l > 0.0f ? 1.0f / c.l : 0.0f;
+        float x0 = c.a0 * inv, x1 = c.a1 * inv;
+        x0 = x0 > 0.0f ? x0 : expm1f(x0);
+        x1 = x1 > 0.0f ? x1 : expm1f(x1);
+        if (store) reinterpret_cast<uint32_t *>(out + (int64_t)v * 64)[lane] = ptx::pack_bf16x2(x0, x1);
+    }
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
+        reinterpret_cast<float4 *>(slot)[lane] = make_float4(c.m, c.l, c.a0, c.a1);
+    }
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
+        const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot) + lane);
+        const float mn = fmaxf(c.m, x.x);
+        if (mn == -INFINITY) return;
+        const float co = __expf(c.m - mn), cp = __expf(x.x - mn);
+        c.l = c.l * co + x.y * cp;
+        c.a0 = c.a0 * co + x.z * cp;
+        c.a1 = c.a1 * co + x.w * cp;
+        c.m = mn;
+    }
+};
+
 // C4: per-edge-type sums of fp32 rows (4 floats per lane, 4 type slots).
 struct TypedF32Op {
     static constexpr int kWin = 0;
+    __device__ static int win_col(int) { return 0; }
     struct Acc { float a[4][4]; };
     struct Val { float4 x; };
     const float *H;
@@ -363,6 +422,8 @@ template <typename Op>
 __device__ __forceinline__ float row_rs(const Op &op, int32_t v, int gl) {
     return Op::kWin ? op.row_value(v, Op::kWin == 1 ? 0 : gl % (Op::kWin ? Op::kWin : 1)) : 0.0f;
 }
+// (GatDenseOp's epilogue does not use the row value, so row_rs's column
+// choice is irrelevant for it.)
 
 // Split rows (hubs, rows straddling a task boundary): every task holding part
 // of row r saves its fp32 partial (combined over sub-groups) to its slot, then
@@ -544,11 +605,11 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
 // touch (row windows, head bookkeeping) lives in a per-warp shared record, so
 // the registers go to in-flight rows: U = 8 fits 64 registers without spills
 // (32 warps per SM, 256 rows of 512 B in flight per SM).
-template <int U>
+template <int U, typename Val, int kWinD>
 struct DenseWarp {
-    uint4 park[U][32];
-    int32_t re[32];  // row_end of rows wr .. wr+31
-    float rv[32];    // epilogue scalar of the same rows
+    Val park[U][32];
+    int32_t re[32];        // row_end of rows wr .. wr+31
+    float rv[32 * kWinD];  // per-row values of the same rows (kWinD per row)
     int32_t wr, v0, row_beg, head_beg, head_end, head;
 };
 
@@ -557,12 +618,12 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
                                                                 const AggWorkspace ws, const int32_t slot_floats,
                                                                 const int dbg) {
     constexpr int kWin = Op::kWin;
-    static_assert(kWin <= 1, "dense engine supports per-row scalars only");
+    constexpr int kWinD = kWin ? kWin : 1;
     static_assert(32 % U == 0, "U must divide the 32-edge chunk");
-    static_assert(sizeof(typename Op::Val) == 16, "dense engine parks 16-byte records");
-    __shared__ DenseWarp<U> warps[kWarpsPerBlock];
-    DenseWarp<U> &W = warps[threadIdx.x >> 5];
-    volatile DenseWarp<U> &VW = W;
+    using DW = DenseWarp<U, typename Op::Val, kWinD>;
+    __shared__ DW warps[kWarpsPerBlock];
+    DW &W = warps[threadIdx.x >> 5];
+    volatile DW &VW = W;
     const int lane = threadIdx.x & 31;
     const int64_t k = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (k >= g.ntasks) return;
@@ -576,7 +637,14 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
         const int32_t r = wbase + lane;
         const bool in = r < g.n;
         VW.re[lane] = in ? (int32_t)__ldg(g.row_ptr + r + 1) : g.e;
-        VW.rv[lane] = (kWin && in) ? op.row_value(r, 0) : 0.0f;
+        if (kWin) {
+#pragma unroll
+            for (int j = 0; j < kWinD; ++j) {  // value (i % kWinD) of row wbase + i / kWinD
+                const int i = j * 32 + lane;
+                const int32_t rr = wbase + i / kWinD;
+                VW.rv[i] = rr < g.n ? op.row_value(rr, i % kWinD) : 0.0f;
+            }
+        }
         if (lane == 0) VW.wr = wbase;
         __syncwarp();
     };
@@ -590,6 +658,8 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
     }
     fill_window(v);
     int32_t row_end = VW.re[0];
+    // this lane's per-row value (e.g. GAT er[v, head]): column Op::win_col(lane)
+    float rs = kWin ? VW.rv[Op::win_col(lane)] : 0.0f;
 
     typename Op::Acc acc;
     op.zero(acc);
@@ -601,13 +671,14 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
             save_partial(op, acc, ws, slot_floats, 2 * k, lane, 0);
             if (lane == 0) VW.head_end = row_end;
         } else {
-            op.finish(v, acc, VW.rv[v - wr], lane, !(dbg & 1));
+            op.finish(v, acc, rs, lane, !(dbg & 1));
         }
         ++v;
         __syncwarp();
         if (lane == 0) VW.row_beg = row_end;
         if (v - wr == 32) fill_window(wr + 32);
         row_end = VW.re[v - VW.wr];
+        if (kWin) rs = VW.rv[(v - VW.wr) * kWinD + Op::win_col(lane)];
         op.zero(acc);
     };
 
@@ -645,16 +716,16 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
         if ((dbg & 2) || row_end > q + U) {
             // fast path: no row ends inside the batch
 #pragma unroll
-            for (int u = 0; u < U; ++u) op.add(acc, val[u], 0.0f, kTyped ? __shfl_sync(kFull, ct_a, base + u) : 0);
+            for (int u = 0; u < U; ++u) op.add(acc, val[u], rs, kTyped ? __shfl_sync(kFull, ct_a, base + u) : 0);
         } else {
             // slow path: park the batch, reduce edge by edge
 #pragma unroll
-            for (int u = 0; u < U; ++u) W.park[u][lane] = *reinterpret_cast<const uint4 *>(&val[u]);
+            for (int u = 0; u < U; ++u) W.park[u][lane] = val[u];
 #pragma unroll 1
             for (int u = 0; u < U; ++u) {
                 const int32_t t = kTyped ? __shfl_sync(kFull, ct_a, base + u) : 0;
-                const uint4 x = W.park[u][lane];
-                op.add(acc, *reinterpret_cast<const typename Op::Val *>(&x), 0.0f, t);
+                const typename Op::Val x = W.park[u][lane];
+                op.add(acc, x, rs, t);
                 while (v < v1 && row_end == q + u + 1) flush();
             }
         }
@@ -663,7 +734,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce_dense(const GraphVi
         slide(q);
         const int idx = q - cb;
         const int32_t t = kTyped ? __shfl_sync(kFull, ct_a, idx) : 0;
-        op.add(acc, op.load(__shfl_sync(kFull, cs_a, idx), lane), 0.0f, t);
+        op.add(acc, op.load(__shfl_sync(kFull, cs_a, idx), lane), rs, t);
         while (v < v1 && row_end == q + 1) flush();
     }
     if (dbg & 2) return;
@@ -721,7 +792,7 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
     switch (kind) {
         case SAGA_GCN: return (size_t)width;        // one fp32 per feature (f_out bf16 or f_in fp32)
         case SAGA_SAGE: return (size_t)width;
-        case SAGA_GAT: return (size_t)heads * 12;   // (m, l, acc[8]) padded to 12
+        case SAGA_GAT: return (size_t)(heads * 12 > 128 ? heads * 12 : 128);  // 32 lanes x (m, l, a0, a1)
         case SAGA_GATED: return (size_t)4 * width;  // 4 type slots
     }
     return 0;
@@ -773,9 +844,18 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    GatOp op{};
+    if (agg_variant() == 9) {
+        GatOp op{};
+        op.z = z; op.el = el; op.er = er; op.slope = slope; op.out = out;
+        return run<8, 4, false, 3>(g, op, ws, 8 * 12, st);
+    }
+    GatDenseOp op{};
     op.z = z; op.el = el; op.er = er; op.slope = slope; op.out = out;
-    return run<8, 4, false, 3>(g, op, ws, 8 * 12, st);
+    switch (agg_variant()) {
+        case 10: return run_dense<16, false, 3>(g, op, ws, 32 * 4, st);
+        case 11: return run_dense<8, false, 3>(g, op, ws, 32 * 4, st);
+    }
+    return run_dense<8, false, 4>(g, op, ws, 32 * 4, st);
 }
 
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, AggWorkspace ws,
@@ -783,8 +863,14 @@ cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, f
     TypedF32Op op{};
     op.H = H; op.f = f; op.S = S;
     if (f != 128) return cudaErrorInvalidValue;
-    if (g.etype) return run_dense<8, true, 2>(g, op, ws, 4 * f, st);
-    return run_dense<8, false, 2>(g, op, ws, 4 * f, st);
+    if (g.etype) {
+        switch (agg_variant()) {
+            case 13: return run_dense<4, true, 4>(g, op, ws, 4 * f, st);
+            case 14: return run_dense<8, true, 2>(g, op, ws, 4 * f, st);
+        }
+        return run_dense<8, true, 3>(g, op, ws, 4 * f, st);
+    }
+    return run_dense<8, false, 3>(g, op, ws, 4 * f, st);
 }
 
 }  // namespace saga

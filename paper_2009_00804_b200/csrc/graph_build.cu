@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -360,6 +361,7 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     // 6. merge-path schedule: ~ 4 tasks per resident warp of a 148-SM part
     int64_t items = e + (int64_t)n;
     int64_t target = (int64_t)kNumSMs * 64 * 4;
+    if (const char *env = getenv("SAGA_TASK_TARGET")) target = atoll(env);  // development knob
     int64_t T = std::max<int64_t>(32, (items + target - 1) / target);
     g->task_items = T;
     g->ntasks = items > 0 ? (items + T - 1) / T : 0;
