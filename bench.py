@@ -40,6 +40,16 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "edge-feature updates/s"
 
 
+def ncu_traffic(cfg_name, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json, written by scripts/make_profiles.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))[cfg_name][kernel]
+    except Exception:
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -302,17 +312,18 @@ def run_saga(args, cfg):
         n_l, ms_l = prof[dom]
         avg_s = ms_l / n_l / 1e3
         a = alg.get(dom, {"bytes": 0, "flops": 0})
+        traffic = args.traffic if args.traffic is not None else ncu_traffic(cfg.name, dom)
         bound = "tensor" if dom.startswith("gemm") and a["flops"] / max(a["bytes"], 1) > \
             pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9) else "hbm"
         if bound == "hbm":
             ach = a["bytes"] / avg_s / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": ach / pk["hbm_gbs"], "traffic": args.traffic, "kernel": dom,
+                    "frac": ach / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
                     "kernel_ms": avg_s * 1e3, "algorithmic_bytes": a["bytes"], "peak_source": pk["source"]}
         else:
             ach = a["flops"] / avg_s / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": ach / pk["bf16_tflops"], "traffic": args.traffic, "kernel": dom,
+                    "frac": ach / pk["bf16_tflops"], "traffic": traffic, "kernel": dom,
                     "kernel_ms": avg_s * 1e3, "peak_source": pk["source"]}
     kernels = {}
     for k, (n_l, ms_l) in prof.items():
@@ -402,7 +413,8 @@ def main():
                     help="in-edges per oracle sample (bounded CPU work)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per launch of the dominant kernel (profiles/), if known")
+                    help="override: ncu dram bytes per launch of the dominant kernel "
+                         "(default: profiles/ncu_traffic.json)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # timing rule: >= 3 warm-up steps
