@@ -1,0 +1,396 @@
+// gemm_tf32x3.cu -- fp32-accurate ApplyEdge-by-type + ApplyVertex GRU for the
+// gated layer (config C4) on the 5th-gen tensor cores.
+//
+// Paper: GGNN's ApplyVertex is a GRU over the gathered message and the
+// vertex's own embedding (Table 1); the
+// per-edge-type message weight is applied after Gather by linearity
+// (sum_e H[u] W_t(e) = sum_t S_t W_t).  Two GEMMs:
+//   messages:  m[M][128]   = [S_0 || .. || S_{T-1}] . [W_0; ..; W_{T-1}]   (K = 128 T)
+//   gates:     G[M][4x128] = [m || h] . B_gru  with, per hidden unit j, the
+//              columns r_j, z_j (K = 256), gin_j (m rows only), ghn_j (h rows
+//              only), followed by the PyTorch-GRUCell epilogue (reading A15):
+//              h' = (1 - z) tanh(gin + b_in + r (ghn + b_hn)) + z h.
+// The fp32 tolerance (1e-4) rules out single-pass TF32 (~3e-4 normwise), so
+// every product is computed as 3xTF32: x = x_hi + x_lo with x_hi = tf32(x)
+// (round to nearest), and A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi
+// (~2^-21 relative, the A_lo.B_lo term is below fp32 rounding).
+//
+// Kernel (persistent, one CTA per SM, 320 threads):
+//   warp 0      TMA producer: per 32-wide K block, the fp32 A tile (128 rows,
+//               128-byte swizzle; A may come from two tensors along K) and the
+//               pre-split B_hi / B_lo tiles (BN rows of W^T),
+//   warp 1      TMEM owner + single-thread tcgen05.mma.kind::tf32 issuer
+//               (M = 128, N = BN, K = 8): 3 MMAs per K step,
+//   warps 2..5  converters: A tile -> A_hi (in place) + A_lo (elementwise,
+//               so the swizzled layout is preserved), fence.proxy.async,
+//   warps 6..9  epilogue: tcgen05.ld, then store (messages) or the GRU.
+// The accumulator is double-buffered in TMEM (2 x BN columns) so the
+// epilogue of one tile overlaps the MMAs of the next.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "internal.cuh"
+#include "ptx.cuh"
+
+namespace saga {
+namespace {
+
+constexpr int kThreads = 320;
+constexpr int kBM = 128;
+constexpr int kBK = 32;                     // fp32 per 128-byte swizzle row
+constexpr int kATile = kBM * kBK * 4;       // 16 KB
+constexpr int kSmemLimit = 232448;
+
+enum { EPI_MSG = 0, EPI_GRU = 1 };
+
+template <int BN>
+struct Layout {
+    static constexpr int kBTile = BN * kBK * 4;                 // one of B_hi / B_lo
+    static constexpr int kStage = 2 * kATile + 2 * kBTile;     // A(hi in place), A_lo, B_hi, B_lo
+    static constexpr int kStages = (kSmemLimit - 2048) / kStage > 4 ? 4 : (kSmemLimit - 2048) / kStage;
+    static constexpr int kBytes = 1024 + kStages * kStage + 1024;
+    static_assert(kStages >= 2, "need a double-buffered ring");
+};
+
+struct alignas(8) Bars {
+    uint64_t full[4], conv[4], empty[4], tfull[2], tempty[2];
+    uint32_t tmem_base;
+};
+
+struct GruEpi {
+    const float *h;      // [M][128]
+    const float *b_ih;   // [3][128]
+    const float *b_hh;   // [3][128]
+    float *out;          // [M][128]
+};
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                  const __grid_constant__ CUtensorMap tmBhi, const __grid_constant__ CUtensorMap tmBlo, int64_t M,
+                  int KB, int KB0, int n_tiles, float *__restrict__ msg_out, int ld_out, GruEpi gru) {
+    using L = Layout<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars *bar = reinterpret_cast<Bars *>(smem + L::kStages * L::kStage);
+    auto stage_a = [&](int s) { return smem + s * L::kStage; };
+    auto stage_alo = [&](int s) { return smem + s * L::kStage + kATile; };
+    auto stage_bhi = [&](int s) { return smem + s * L::kStage + 2 * kATile; };
+    auto stage_blo = [&](int s) { return smem + s * L::kStage + 2 * kATile + L::kBTile; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m_tiles = (M + kBM - 1) / kBM;
+    const int64_t ntiles = m_tiles * n_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < L::kStages; ++s) {
+            ptx::mbar_init(&bar->full[s], 1);
+            ptx::mbar_init(&bar->conv[s], 128);
+            ptx::mbar_init(&bar->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&bar->tfull[a], 1);
+            ptx::mbar_init(&bar->tempty[a], 128);
+        }
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmA0);
+        ptx::prefetch_tmap(&tmA1);
+        ptx::prefetch_tmap(&tmBhi);
+        ptx::prefetch_tmap(&tmBlo);
+    }
+    if (warp == 1) ptx::tmem_alloc<2 * BN>(&bar->tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        if (lane == 0) {
+            const uint64_t pol_a = ptx::policy_evict_first();  // A streamed once
+            const uint64_t pol_b = ptx::policy_evict_last();   // B re-read by every CTA
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int32_t m0 = (int32_t)((t / n_tiles) * kBM);
+                const int32_t n0 = (int32_t)((t % n_tiles) * BN);
+                for (int kb = 0; kb < KB; ++kb) {
+                    ptx::mbar_wait(&bar->empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&bar->full[stage], kATile + 2 * L::kBTile);
+                    const bool first = kb < KB0;
+                    ptx::tma_load_2d(stage_a(stage), first ? &tmA0 : &tmA1, &bar->full[stage],
+                                     (first ? kb : kb - KB0) * kBK, m0, pol_a);
+                    ptx::tma_load_2d(stage_bhi(stage), &tmBhi, &bar->full[stage], kb * kBK, n0, pol_b);
+                    ptx::tma_load_2d(stage_blo(stage), &tmBlo, &bar->full[stage], kb * kBK, n0, pol_b);
+                    if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ==============================
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::make_idesc(2 /*TF32*/, kBM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(&bar->tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < KB; ++kb) {
+                    ptx::mbar_wait(&bar->conv[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t ahi = ptx::smem_u32(stage_a(stage)), alo = ptx::smem_u32(stage_alo(stage));
+                    const uint32_t bhi = ptx::smem_u32(stage_bhi(stage)), blo = ptx::smem_u32(stage_blo(stage));
+#pragma unroll
+                    for (int k = 0; k < kBK / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
+                        const uint32_t off = k * 32;
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(bhi + off), idesc,
+                                       (kb | k) != 0);
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + off), idesc, 1);
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(bhi + off), idesc, 1);
+                    }
+                    ptx::umma_commit(&bar->empty[stage]);  // frees the stage when these MMAs retire
+                    if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(&bar->tfull[acc]);
+            }
+        }
+    } else if (warp < 6) {
+        // ============================ converters ==============================
+        const int ct = threadIdx.x - 64;  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int kb = 0; kb < KB; ++kb) {
+                ptx::mbar_wait(&bar->full[stage], phase);
+                float4 *a = reinterpret_cast<float4 *>(stage_a(stage));
+                float4 *lo = reinterpret_cast<float4 *>(stage_alo(stage));
+#pragma unroll
+                for (int i = 0; i < kATile / 16 / 128; ++i) {
+                    const int c = i * 128 + ct;
+                    const float4 x = a[c];
+                    const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+                    a[c] = h;
+                    lo[c] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                }
+                ptx::fence_proxy_async_smem();  // generic writes -> visible to the tensor core
+                ptx::mbar_arrive(&bar->conv[stage]);
+                if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ============================ epilogue ================================
+        const int q = warp & 3;       // TMEM lane quarter this warp may access
+        const int r = q * 32 + lane;  // row within the tile
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            const int64_t row = (t / n_tiles) * kBM + r;
+            const int nt = (int)(t % n_tiles);
+            ptx::mbar_wait(&bar->tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+            if (EPI == EPI_MSG) {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tbase + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (row < M) {
+                        float4 *o = reinterpret_cast<float4 *>(msg_out + row * ld_out + nt * BN + c * 32);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                    }
+                }
+            } else {
+                // tile columns: [r | z | gin | ghn] x 64 units (unit0 = 64 nt)
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t vr[32], vz[32];
+                    ptx::tmem_ld32(tbase + c * 32, vr);
+                    ptx::tmem_ld32(tbase + 64 + c * 32, vz);
+                    ptx::tmem_ld_wait();
+                    const int j0 = nt * 64 + c * 32;
+                    float rg[32], zg[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        rg[j] = sigmoidf_(__uint_as_float(vr[j]) + __ldg(gru.b_ih + j0 + j) + __ldg(gru.b_hh + j0 + j));
+                        zg[j] = sigmoidf_(__uint_as_float(vz[j]) + __ldg(gru.b_ih + 128 + j0 + j) +
+                                          __ldg(gru.b_hh + 128 + j0 + j));
+                    }
+                    uint32_t vi[32], vh[32];
+                    ptx::tmem_ld32(tbase + 128 + c * 32, vi);
+                    ptx::tmem_ld32(tbase + 192 + c * 32, vh);
+                    ptx::tmem_ld_wait();
+                    if (row < M) {
+                        const float4 *hp = reinterpret_cast<const float4 *>(gru.h + row * 128 + j0);
+                        float4 *op = reinterpret_cast<float4 *>(gru.out + row * 128 + j0);
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4) {
+                            const float4 hv = __ldg(hp + j4);
+                            const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
+                            float o[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int j = 4 * j4 + e;
+                                const float n = tanhf(__uint_as_float(vi[j]) + __ldg(gru.b_ih + 256 + j0 + j) +
+                                                      rg[j] * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
+                                o[e] = (1.0f - zg[j]) * n + zg[j] * hh[e];
+                            }
+                            op[j4] = make_float4(o[0], o[1], o[2], o[3]);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&bar->tempty[acc]);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<2 * BN>(tmem);
+    }
+}
+
+// B^T operands in K-major layout, split hi/lo:
+//   messages: Bm[n][k] = W_type[k / f][k % f][n]             (N = f, K = T f)
+//   gates:    Bg[c][k], c = 256 nt + 64 g + j (unit 64 nt + j; g = r, z, gin, ghn),
+//             k < f from W_ih, k >= f from W_hh; gin has no h rows, ghn no m rows.
+__global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_ih,
+                                const float *__restrict__ W_hh, float *bm_hi, float *bm_lo, float *bg_hi,
+                                float *bg_lo) {
+    const int nm = f * T * f, ng = 4 * f * 2 * f;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nm + ng; i += gridDim.x * blockDim.x) {
+        float x;
+        float *hi, *lo;
+        int idx;
+        if (i < nm) {
+            const int n = i / (T * f), k = i % (T * f);
+            x = W_type[((int64_t)(k / f) * f + k % f) * f + n];
+            hi = bm_hi; lo = bm_lo; idx = i;
+        } else {
+            idx = i - nm;
+            const int c = idx / (2 * f), k = idx % (2 * f);
+            const int nt = c / 256, g = (c % 256) / 64, j = nt * 64 + c % 64;
+            const bool from_m = k < f;
+            const int kk = from_m ? k : k - f;
+            if (g < 2)
+                x = (from_m ? W_ih : W_hh)[((int64_t)g * f + kk) * f + j];
+            else if (g == 2)
+                x = from_m ? W_ih[((int64_t)2 * f + kk) * f + j] : 0.0f;
+            else
+                x = from_m ? 0.0f : W_hh[((int64_t)2 * f + kk) * f + j];
+            hi = bg_hi; lo = bg_lo;
+        }
+        const float h = tf32_rna(x);
+        hi[idx] = h;
+        lo[idx] = x - h;
+    }
+}
+
+// ------------------------------------------------------------- host side ----
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// 2-D fp32 row-major [rows][cols] (row stride ld floats) with a {32, box_rows} box, 128B swizzle.
+bool make_map_f32(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+cudaError_t launch_tf32x3(const CUtensorMap &a0, const CUtensorMap &a1, const CUtensorMap &bhi,
+                          const CUtensorMap &blo, int64_t M, int KB, int KB0, int n_tiles, float *msg_out, int ld_out,
+                          const GruEpi &gru, cudaStream_t st) {
+    using L = Layout<BN>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tf32x3<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             L::kBytes);
+        if (e) return e;
+        attr = true;
+    }
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (M + kBM - 1) / kBM * n_tiles;
+    const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
+    k_gemm_tf32x3<BN, EPI><<<grid, kThreads, L::kBytes, st>>>(a0, a1, bhi, blo, M, KB, KB0, n_tiles, msg_out, ld_out,
+                                                                gru);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t gated_tc_workspace_floats(int32_t f, int32_t T) { return (size_t)2 * f * T * f + (size_t)2 * 4 * f * 2 * f; }
+
+cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
+                                  const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
+                                  const float *b_hh, float *m_ws, float *wsplit, float *out, cudaStream_t st,
+                                  const char **why) {
+    if (M == 0) return cudaSuccess;
+    if (f != 128 || T < 1 || T > 4) {
+        *why = "tensor-core gated path needs f = 128, 1 <= T <= 4";
+        return cudaErrorInvalidValue;
+    }
+    float *bm_hi = wsplit, *bm_lo = bm_hi + (size_t)f * T * f;
+    float *bg_hi = bm_lo + (size_t)f * T * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
+    k_split_weights<<<256, 256, 0, st>>>(f, T, W_type, W_ih, W_hh, bm_hi, bm_lo, bg_hi, bg_lo);
+    cudaError_t e = cudaGetLastError();
+    if (e) return e;
+    CUtensorMap aS, aM, aH, bmh, bml, bgh, bgl;
+    if (!make_map_f32(&aS, S, M, (int64_t)T * f, 4 * f, kBM) || !make_map_f32(&aM, m_ws, M, f, f, kBM) ||
+        !make_map_f32(&aH, H, M, f, f, kBM) || !make_map_f32(&bmh, bm_hi, f, (int64_t)T * f, (int64_t)T * f, 128) ||
+        !make_map_f32(&bml, bm_lo, f, (int64_t)T * f, (int64_t)T * f, 128) ||
+        !make_map_f32(&bgh, bg_hi, 4 * f, 2 * f, 2 * f, 256) || !make_map_f32(&bgl, bg_lo, 4 * f, 2 * f, 2 * f, 256)) {
+        *why = "cuTensorMapEncodeTiled failed";
+        return cudaErrorInvalidValue;
+    }
+    GruEpi none{nullptr, nullptr, nullptr, nullptr};
+    e = launch_tf32x3<128, EPI_MSG>(aS, aS, bmh, bml, M, T * f / kBK, T * f / kBK, 1, m_ws, f, none, st);
+    if (e) return e;
+    GruEpi gru{H, b_ih, b_hh, out};
+    return launch_tf32x3<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
+}
+
+}  // namespace saga

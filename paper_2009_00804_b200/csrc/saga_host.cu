@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <mutex>
@@ -142,6 +143,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GATED:
             p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S
             p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
+            p.inter2 = align_up(sizeof(float) * saga::gated_tc_workspace_floats(128, 4));       // split W
             break;
     }
     p.total = p.counters + p.partials + p.inter0 + p.inter1 + p.inter2;
@@ -400,12 +402,20 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, aw, st);
             }
             if (e) return cuda_fail(e, "typed aggregate");
-            {
+            if (getenv("SAGA_GATED_SIMT")) {  // development knob: the FFMA reference kernels
                 ProfScope ps_("gated_apply_sgemm", st);
                 e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
                                    w->W_ih, w->W_hh, w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
+                if (e) return cuda_fail(e, "gated apply");
+                return SAGA_OK;
             }
-            if (e) return cuda_fail(e, "gated apply");
+            {
+                ProfScope ps_("gated_apply_tf32x3", st);
+                e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data),
+                                          w->W_type, w->W_ih, w->W_hh, w->b_ih, w->b_hh, m,
+                                          reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "gated apply: %s (%s)", cudaGetErrorString(e), why);
             return SAGA_OK;
         }
     }
