@@ -113,31 +113,61 @@ class ClockSampler:
 
 # ------------------------------------------------------------- byte model ----
 def algorithmic(cfg):
-    """Algorithmic (compulsory) bytes and FLOPs per launch of each kernel
-    (DESIGN.md "Roofline"): every array the kernel must touch, once."""
+    """Algorithmic (compulsory) bytes and FLOPs PER LAUNCH of each kernel
+    (DESIGN.md section 5): every array the kernel must touch, once; FLOPs are
+    the layer's own arithmetic counted once.  `peak` names the roofline the
+    kernel is held to: "hbm", or "tensor_bf16" / "tensor_tf32x3" (3xTF32: the
+    fp32-accurate product costs three TF32 MMAs, so its peak is TF32 / 3)."""
     n, e = cfg.n, cfg.num_edges
     out = {}
     if cfg.model == "gcn" and cfg.dtype == "bf16":
         fi, fo = cfg.dims
-        out["gemm_bf16_tc"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * 4 + n * fo * 2, "flops": 2 * n * fi * fo}
-        out["agg_gcn_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 4 + n * fo * 2, "flops": e * fo}
+        out["gemm_bf16_tc"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * 4 + n * fo * 2, "flops": 2 * n * fi * fo,
+                               "peak": "tensor_bf16"}
+        out["agg_gcn_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 4 + n * fo * 2, "flops": e * fo,
+                               "peak": "hbm"}
     elif cfg.model == "gcn":
         fi, fo = cfg.dims
         out["gcn_f32_fused"] = {"bytes": e * 4 + (n + 1) * 8 + n * fi * 4 + n * 4 + n * fo * 4,
-                                "flops": 2 * e * fi + 2 * n * fi * fo}
+                                "flops": 2 * e * fi + 2 * n * fi * fo, "peak": "hbm"}
     elif cfg.model == "sage":
-        f0, f1, f2 = cfg.dims
-        out["agg_mean_bf16"] = {"bytes": 2 * (e * 4 + (n + 1) * 8) + n * (f0 + f1) * 2 * 2, "flops": e * (f0 + f1)}
-        out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f0 + f1 + 2 * f1 + f2), "flops": 2 * n * (2 * f0 * f1 + 2 * f1 * f2)}
+        f0, f1, f2 = cfg.dims   # two layers: agg widths f0, f1; GEMMs 2f0 -> f1, 2f1 -> f2 (mean of the two launches)
+        out["agg_mean_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * 4 + n * (f0 + f1) * 2 * 2 // 2,
+                                "flops": e * (f0 + f1) // 2, "peak": "hbm"}
+        out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f0 + f1 + 2 * f1 + f2) // 2,
+                               "flops": 2 * n * (2 * f0 * f1 + 2 * f1 * f2) // 2, "peak": "tensor_bf16"}
     elif cfg.model == "gat":
         fi, fo = cfg.dims
-        out["gemm_bf16_tc_gat"] = {"bytes": n * fi * 2 + n * fo * 2 + n * 64, "flops": 2 * n * fi * fo}
-        out["gat_edge"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 64 + n * fo * 2, "flops": 10 * e * fo}
+        out["gemm_bf16_tc_gat"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * fo * 2 + n * 64, "flops": 2 * n * fi * fo,
+                                   "peak": "tensor_bf16"}
+        out["gat_edge"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 64 + n * fo * 2, "flops": 10 * e * fo,
+                           "peak": "hbm"}
     elif cfg.model == "gated":
-        f = cfg.dims[0]
-        out["agg_typed_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f}
-        out["gated_apply_sgemm"] = {"bytes": n * 4 * f * 4 + n * f * 4 * 3, "flops": 2 * n * (4 * f * f + 6 * f * f)}
+        f, T = cfg.dims[0], cfg.num_etypes
+        out["agg_typed_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f,
+                                "peak": "hbm"}
+        # S read, m written + read, h read twice (GEMM A operand, GRU epilogue), h' written
+        out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
+                                     "peak": "tensor_tf32x3"}
+        out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x3"], peak="hbm")
     return out
+
+
+def roofline_of(name, spec, avg_s, pk, traffic):
+    """roofline object of the bench line for kernel `name`."""
+    base = {"kernel": name, "kernel_ms": avg_s * 1e3, "traffic": traffic,
+            "algorithmic_bytes": spec["bytes"], "algorithmic_flops": spec["flops"], "peak_source": pk["source"]}
+    if spec["peak"] == "hbm":
+        ach = spec["bytes"] / avg_s / 1e9
+        return dict(base, bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"])
+    # tensor: bf16 measured burst peak; TF32 = bf16 x (1.1 / 2.25 nominal ratio); 3xTF32 = TF32 / 3
+    peak = pk["bf16_tflops"]
+    note = "measured bf16 burst"
+    if spec["peak"] == "tensor_tf32x3":
+        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
+        note = "measured bf16 burst x nominal tf32/bf16 (1.1/2.25) / 3 (3xTF32)"
+    ach = spec["flops"] / avg_s / 1e12
+    return dict(base, bound="tensor", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak, peak_note=note)
 
 
 # --------------------------------------------------------------- helpers ----
@@ -303,34 +333,24 @@ def run_saga(args, cfg):
     value = upd_step * args.steps * ws / (tot_ms / 1e3)
     launches = sum(n for n, _ in prof.values())
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (largest share of the step)
     alg = algorithmic(cfg)
     pk = peaks()
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
     roof = None
-    if dom:
+    if dom and dom in alg:
         n_l, ms_l = prof[dom]
-        avg_s = ms_l / n_l / 1e3
-        a = alg.get(dom, {"bytes": 0, "flops": 0})
         traffic = args.traffic if args.traffic is not None else ncu_traffic(cfg.name, dom)
-        bound = "tensor" if dom.startswith("gemm") and a["flops"] / max(a["bytes"], 1) > \
-            pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9) else "hbm"
-        if bound == "hbm":
-            ach = a["bytes"] / avg_s / 1e9
-            roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": ach / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
-                    "kernel_ms": avg_s * 1e3, "algorithmic_bytes": a["bytes"], "peak_source": pk["source"]}
-        else:
-            ach = a["flops"] / avg_s / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": ach / pk["bf16_tflops"], "traffic": traffic, "kernel": dom,
-                    "kernel_ms": avg_s * 1e3, "peak_source": pk["source"]}
+        roof = roofline_of(dom, alg[dom], ms_l / n_l / 1e3, pk, traffic)
     kernels = {}
     for k, (n_l, ms_l) in prof.items():
         a = alg.get(k, {"bytes": 0, "flops": 0})
         avg = ms_l / n_l
         kernels[k] = {"launches": n_l, "avg_ms": avg, "share": ms_l / tot_ms if ws == 1 else None,
                       "alg_GBps": a["bytes"] / (avg / 1e3) / 1e9, "alg_TFLOPs": a["flops"] / (avg / 1e3) / 1e12}
+        if k in alg:
+            r = roofline_of(k, alg[k], avg / 1e3, pk, ncu_traffic(cfg.name, k))
+            kernels[k].update({"bound": r["bound"], "frac": r["frac"], "traffic": r["traffic"]})
 
     # end to end through the public API with host buffers
     e2e = run_e2e(args, cfg, saga, H, d, dev, ws) if args.e2e_steps > 0 else None

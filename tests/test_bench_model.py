@@ -1,0 +1,59 @@
+"""bench.py's roofline model (CPU): per-launch algorithmic bytes/FLOPs and
+the roofline object."""
+import importlib.util
+import os
+
+import pytest
+
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def test_c5_aggregation_compulsory_bytes(bench):
+    c = W.CONFIGS["C5"]
+    a = bench.algorithmic(c)["agg_gcn_bf16"]
+    n, e = 1 << 22, (1 << 26) + (1 << 22)
+    # col_src once, row_ptr once, Y (bf16 256) once, dinv once, out (bf16 256) once
+    assert a["bytes"] == 4 * e + 8 * (n + 1) + 512 * n + 4 * n + 512 * n
+    assert a["peak"] == "hbm"
+    g = bench.algorithmic(c)["gemm_bf16_tc"]
+    assert g["flops"] == 2 * n * 256 * 256
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
+def test_every_profiled_kernel_has_a_model(bench, cfg):
+    expected = {"C1": {"gcn_f32_fused"}, "C2": {"agg_mean_bf16", "gemm_bf16_tc"},
+                "C3": {"gemm_bf16_tc_gat", "gat_edge"}, "C4": {"agg_typed_f32", "gated_apply_tf32x3"},
+                "C5": {"gemm_bf16_tc", "agg_gcn_bf16"}}[cfg]
+    alg = bench.algorithmic(W.CONFIGS[cfg])
+    assert expected <= set(alg)
+    for k in expected:
+        assert alg[k]["bytes"] > 0 and alg[k]["flops"] > 0
+
+
+def test_sage_model_is_per_launch(bench):
+    """Two layers -> two launches per kernel per step: the model is the mean."""
+    c = W.CONFIGS["C2"]
+    n, e = c.n, c.num_edges
+    a = bench.algorithmic(c)["agg_mean_bf16"]
+    one = e * 4 + (n + 1) * 8 + n * 4 + 2 * n * 128 * 2   # width 128 both layers: X read + M written
+    assert a["bytes"] == one
+
+
+def test_roofline_object(bench):
+    pk = {"hbm_gbs": 6500.0, "bf16_tflops": 1650.0, "bf16_tflops_sustained": 1390.0, "source": "measured"}
+    r = bench.roofline_of("k", {"bytes": 6.5e9, "flops": 1, "peak": "hbm"}, 2e-3, pk, 1.0e10)
+    assert r["bound"] == "hbm" and abs(r["achieved"] - 3250.0) < 1e-6 and abs(r["frac"] - 0.5) < 1e-12
+    assert r["traffic"] == 1.0e10
+    t = bench.roofline_of("k", {"bytes": 1, "flops": 1e12, "peak": "tensor_tf32x3"}, 1e-2, pk, None)
+    assert t["bound"] == "tensor" and abs(t["peak"] - 1650.0 * 1.1 / 2.25 / 3) < 1e-9
+    assert abs(t["achieved"] - 100.0) < 1e-9
