@@ -166,6 +166,11 @@ def roofline_of(name, spec, avg_s, pk, traffic):
     if spec["peak"] == "tensor_tf32x3":
         peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
         note = "measured bf16 burst x nominal tf32/bf16 (1.1/2.25) / 3 (3xTF32)"
+    # a contraction whose bytes take longer than its FLOPs is HBM-bound
+    if spec["bytes"] / (pk["hbm_gbs"] * 1e9) > spec["flops"] / (peak * 1e12):
+        ach = spec["bytes"] / avg_s / 1e9
+        return dict(base, bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"],
+                    peak_note="arithmetic intensity below the ridge of " + note)
     ach = spec["flops"] / avg_s / 1e12
     return dict(base, bound="tensor", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak, peak_note=note)
 

@@ -57,3 +57,13 @@ def test_roofline_object(bench):
     t = bench.roofline_of("k", {"bytes": 1, "flops": 1e12, "peak": "tensor_tf32x3"}, 1e-2, pk, None)
     assert t["bound"] == "tensor" and abs(t["peak"] - 1650.0 * 1.1 / 2.25 / 3) < 1e-9
     assert abs(t["achieved"] - 100.0) < 1e-9
+
+
+def test_hbm_bound_contraction_is_held_to_hbm(bench):
+    """C5's pre-projection GEMM (128 FLOP/B) sits below the bf16 ridge."""
+    pk = {"hbm_gbs": 6536.0, "bf16_tflops": 1653.2, "bf16_tflops_sustained": 1391.2, "source": "measured"}
+    spec = bench.algorithmic(W.CONFIGS["C5"])["gemm_bf16_tc"]
+    r = bench.roofline_of("gemm_bf16_tc", spec, 0.7e-3, pk, None)
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    c4 = bench.algorithmic(W.CONFIGS["C4"])["gated_apply_tf32x3"]
+    assert bench.roofline_of("g", c4, 0.36e-3, pk, None)["bound"] == "tensor"
