@@ -40,6 +40,7 @@ constexpr int kSmemLimit = 232448;            // 227 KB opt-in maximum
 struct alignas(8) Barriers {
     uint64_t full[8], empty[8], tfull[2], tempty[2];
     uint32_t tmem_base;
+    float vec[256];  // epilogue vectors staged once per CTA: bias[BN], or GAT a_src[64] | a_dst[64]
 };
 
 template <int BN>
@@ -123,6 +124,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmA0);
         ptx::prefetch_tmap(&tmA1);
         ptx::prefetch_tmap(&tmC);
+    }
+    for (int i = threadIdx.x; i < BN; i += kThreads) {
+        if (ep.epi == EPI_BIAS_ACT) {
+            bar->vec[i] = ep.bias ? ep.bias[i] : 0.0f;
+        } else if (ep.epi == EPI_GAT) {  // BN = 64 here
+            bar->vec[i] = ep.a_src[i];
+            bar->vec[64 + i] = ep.a_dst[i];
+        }
     }
     if (warp == 1) ptx::tmem_alloc<2 * BN>(&bar->tmem_base);
     ptx::fence_proxy_async_smem();  // W written by generic stores, read by UMMA
@@ -217,13 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int i = 0; i < 32; ++i) x[i] *= scale;
                     } else if (ep.epi == EPI_BIAS_ACT) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) x[i] = act_fn(x[i] + (ep.bias ? __ldg(ep.bias + col0 + i) : 0.0f), ep.act);
+                        for (int i = 0; i < 32; ++i) x[i] = act_fn(x[i] + bar->vec[col0 + i], ep.act);
                     } else {  // EPI_GAT: heads of 8 columns; el/er from the fp32 accumulators
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
                             const int h = (half * 32 + i) >> 3;  // GAT runs with BN = 64 (c64 == 0)
-                            el[h] = fmaf(x[i], __ldg(ep.a_src + col0 + i), el[h]);
-                            er[h] = fmaf(x[i], __ldg(ep.a_dst + col0 + i), er[h]);
+                            el[h] = fmaf(x[i], bar->vec[col0 + i], el[h]);
+                            er[h] = fmaf(x[i], bar->vec[64 + col0 + i], er[h]);
                         }
                     }
 #pragma unroll
