@@ -81,7 +81,7 @@ typedef struct {
     int32_t heads, head_dim;  /* GAT only (else ignored)                                  */
     int32_t act;              /* saga_act applied by ApplyVertex: GCN/SAGE (RELU or NONE); */
                               /* GAT must be ELU; GATED ignores it (GRU)                   */
-    float leaky_slope;        /* GAT LeakyReLU negative slope (0.2 in config C3)          */
+    float leaky_slope;        /* GAT LeakyReLU negative slope in [0, 1] (0.2 in config C3) */
 } saga_layer_opts;
 
 /* Weights (device, row-major, [in][out] orientation = x . W, reading A8).

@@ -241,9 +241,9 @@ struct GatOp {
     }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h, int32_t) const {
         float s = v.el + er_h;
-        s = s > 0.0f ? s : slope * s;
+        s = fmaxf(s, slope * s);                 // LeakyReLU for 0 <= slope <= 1
         const float d = s - c.m;                 // +inf for the first term
-        const float e = __expf(-fabsf(d));       // 0 for the first term
+        const float e = ptx::exp2_ftz(-fabsf(d) * 1.4426950408889634f);  // exp(-|d|); 0 for the first term
         const bool up = d > 0.0f;
         const float co = up ? e : 1.0f, cn = up ? 1.0f : e;
         const float2 f = ptx::unpack_bf16x2(v.z2);

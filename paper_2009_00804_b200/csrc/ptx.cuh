@@ -225,6 +225,13 @@ __device__ __forceinline__ void stg_v4_stream(void *p, uint4 v) {
         : "memory");
 }
 
+// 2^x on the SFU, flush-to-zero (one MUFU.EX2, no range fix-up).
+__device__ __forceinline__ float exp2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // acc[0..1] += the two bf16 halves of `u`, in fp32 (sm_100 mixed-precision
 // add: one FHADD.BF16 per element, no unpacking).
 __device__ __forceinline__ void add_bf16x2_f32(float &lo, float &hi, uint32_t u) {

@@ -370,6 +370,8 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (o.heads != 8 || o.head_dim != 8 || o.out_dim != 64 || o.in_dim % 64 || o.in_dim > 256 || !o.in_dim)
                 return fail(SAGA_EUNSUPPORTED, "GAT supports heads=8, head_dim=8, in_dim in {64..256 step 64}");
             if (o.act != SAGA_ACT_ELU) return fail(SAGA_EUNSUPPORTED, "GAT act must be ELU");
+            if (!(o.leaky_slope >= 0.0f && o.leaky_slope <= 1.0f))
+                return fail(SAGA_EUNSUPPORTED, "GAT leaky_slope must lie in [0, 1]");
             __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(i0);
             float *el = reinterpret_cast<float *>(i1), *er = reinterpret_cast<float *>(i2);
             GemmArgs a;
