@@ -152,9 +152,9 @@ struct SumBf16Op {
 template <int NPL>
 struct GcnF32FusedOp {
     static constexpr int kWin = 1;
-    static constexpr int kSlot = 32 * NPL;
+    static constexpr int kSlot = 2 * 32 * NPL;  // doubles as float pairs
     __device__ static int win_col(int) { return 0; }
-    struct Acc { float a[NPL]; };
+    struct Acc { double a[NPL]; };  // fp64 accumulation (see TypedF32Op)
     struct Val { float x[NPL]; float w; };
     const float *X;
     int32_t f_in, f_out;
@@ -185,12 +185,12 @@ struct GcnF32FusedOp {
     }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float, int32_t) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c.a[i] = fmaf(v.w, v.x[i], c.a[i]);
+        for (int i = 0; i < NPL; ++i) c.a[i] = fma((double)v.w, (double)v.x[i], c.a[i]);
     }
     __device__ __forceinline__ void finish_w(int32_t v, const Acc &c, float rs, const float *Ws, int lane) const {
         float h[NPL];
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) h[i] = rs * c.a[i];
+        for (int i = 0; i < NPL; ++i) h[i] = (float)((double)rs * c.a[i]);
         float o0 = 0.0f, o1 = 0.0f;
         const int j0 = lane, j1 = lane + 32;
         for (int kl = 0; kl < f_in / NPL; ++kl) {  // lane kl holds inputs kl*NPL ..
@@ -207,11 +207,11 @@ struct GcnF32FusedOp {
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) slot[lane * NPL + i] = c.a[i];
+        for (int i = 0; i < NPL; ++i) reinterpret_cast<double *>(slot)[lane * NPL + i] = c.a[i];
     }
     __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c.a[i] += __ldcg(slot + lane * NPL + i);
+        for (int i = 0; i < NPL; ++i) c.a[i] += __ldcg(reinterpret_cast<const double *>(slot) + lane * NPL + i);
     }
 };
 
@@ -275,12 +275,15 @@ struct GatOp {
     }
 };
 
-// C4: per-edge-type sums of fp32 rows (4 floats per lane, 4 type slots).
+// C4: per-edge-type sums of fp32 rows (4 floats per lane, 4 type slots),
+// accumulated in fp64: a 70K-edge hub summed in fp32 loses ~1e-4 of the
+// normwise output accuracy through the GRU (the fp32 configs' tolerance),
+// while FP64 adds cost nothing on this memory-bound loop.
 struct TypedF32Op {
     static constexpr int kWin = 0;
-    static constexpr int kSlot = 4 * 128;
+    static constexpr int kSlot = 2 * 4 * 128;  // doubles as float pairs
     __device__ static int win_col(int) { return 0; }
-    struct Acc { float a[4][4]; };
+    struct Acc { double a[4][4]; };
     struct Val { float4 x; };
     const float *H;
     float *S;  // [n][4][128]
@@ -289,7 +292,7 @@ struct TypedF32Op {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) c.a[t][i] = 0.0f;
+            for (int i = 0; i < 4; ++i) c.a[t][i] = 0.0;
     }
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
         const char *p = reinterpret_cast<const char *>(H) + lane * 16 + (uint64_t)(uint32_t)u * 512u;
@@ -299,29 +302,36 @@ struct TypedF32Op {
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt)
             if (t == tt) {
-                c.a[tt][0] += v.x.x;
-                c.a[tt][1] += v.x.y;
-                c.a[tt][2] += v.x.z;
-                c.a[tt][3] += v.x.w;
+                c.a[tt][0] += (double)v.x.x;
+                c.a[tt][1] += (double)v.x.y;
+                c.a[tt][2] += (double)v.x.z;
+                c.a[tt][3] += (double)v.x.w;
             }
     }
     __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             reinterpret_cast<float4 *>(S + ((int64_t)v * 4 + t) * 128)[lane] =
-                make_float4(c.a[t][0], c.a[t][1], c.a[t][2], c.a[t][3]);
+                make_float4((float)c.a[t][0], (float)c.a[t][1], (float)c.a[t][2], (float)c.a[t][3]);
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
+        double *d = reinterpret_cast<double *>(slot);
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            reinterpret_cast<float4 *>(slot + t * 128)[lane] = make_float4(c.a[t][0], c.a[t][1], c.a[t][2], c.a[t][3]);
+#pragma unroll
+            for (int i = 0; i < 4; i += 2)
+                reinterpret_cast<double2 *>(d + t * 128 + lane * 4)[i / 2] = make_double2(c.a[t][i], c.a[t][i + 1]);
     }
     __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
+        const double *d = reinterpret_cast<const double *>(slot);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot + t * 128) + lane);
-            c.a[t][0] += x.x; c.a[t][1] += x.y; c.a[t][2] += x.z; c.a[t][3] += x.w;
-        }
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < 4; i += 2) {
+                const double2 x = __ldcg(reinterpret_cast<const double2 *>(d + t * 128 + lane * 4) + i / 2);
+                c.a[t][i] += x.x;
+                c.a[t][i + 1] += x.y;
+            }
     }
 };
 
@@ -544,7 +554,7 @@ template <int NPL>
 cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                     const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st) {
     GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
-    return run<8, false, 3>(g, op, ws, st, W, f_in * f_out);
+    return run<8, false, NPL == 4 ? 2 : 3>(g, op, ws, st, W, f_in * f_out);
 }
 
 }  // namespace
@@ -552,10 +562,10 @@ cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float
 size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
     (void)heads;
     switch (kind) {
-        case SAGA_GCN: return (size_t)(width > 32 ? width : 32);  // 32 lanes x (1..8) fp32
+        case SAGA_GCN: return (size_t)2 * (width > 32 ? width : 32);  // 32 lanes x (1..8) fp32, or fp64 (fp32 path)
         case SAGA_SAGE: return (size_t)(width > 32 ? width : 32);
         case SAGA_GAT: return 128;                                // 32 lanes x (m, l, a0, a1)
-        case SAGA_GATED: return (size_t)4 * 128;                  // 4 type slots x 128
+        case SAGA_GATED: return (size_t)2 * 4 * 128;              // 4 type slots x 128 fp64
     }
     return 0;
 }
@@ -592,8 +602,10 @@ cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, f
                                  cudaStream_t st) {
     if (f != 128) return cudaErrorInvalidValue;
     TypedF32Op op{H, S};
-    if (g.etype) return run<8, true, 3>(g, op, ws, st);
-    return run<8, false, 3>(g, op, ws, st);
+    // fp64 accumulators leave room for U = 4 at 64 registers (32 warps/SM),
+    // measured faster than U = 8 at 2-3 blocks/SM
+    if (g.etype) return run<4, true, 4>(g, op, ws, st);
+    return run<4, false, 4>(g, op, ws, st);
 }
 
 }  // namespace saga

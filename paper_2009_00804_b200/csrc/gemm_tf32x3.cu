@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        (kb | k) != 0);
                         ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + off), idesc, 1);
                         ptx::umma_tf32(d, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(bhi + off), idesc, 1);
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(blo + off), idesc, 1);
                     }
                     ptx::umma_commit(&bar->empty[stage]);  // frees the stage when these MMAs retire
                     if (++stage == L::kStages) { stage = 0; phase ^= 1; }
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float4 x = a[c];
                     const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
                     a[c] = h;
-                    lo[c] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                    lo[c] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
+                                        tf32_rna(x.w - h.w));
                 }
                 ptx::fence_proxy_async_smem();  // generic writes -> visible to the tensor core
                 ptx::mbar_arrive(&bar->conv[stage]);
@@ -303,7 +305,7 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
         }
         const float h = tf32_rna(x);
         hi[idx] = h;
-        lo[idx] = x - h;
+        lo[idx] = tf32_rna(x - h);
     }
 }
 

@@ -129,8 +129,8 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GATED: width = (size_t)o.in_dim; break;
     }
     size_t pf = saga::agg_partial_floats(kind, (int32_t)width, 8);
-    if (kind == SAGA_GCN) pf = (size_t)std::max(o.in_dim, o.out_dim);  // covers the fp32 agg-first path too
-    pf = std::max<size_t>(pf, 32);                                        // >= one fp32 per lane
+    if (kind == SAGA_GCN) pf = (size_t)2 * std::max({o.in_dim, o.out_dim, 32});  // fp64 partials on the fp32 path
+    pf = std::max<size_t>(pf, 32);                                                  // >= one fp32 per lane
     p.counters = align_up(sizeof(int32_t) * (nt + 1));
     p.partials = align_up(sizeof(float) * pf * 2 * (nt + 1));
     switch (kind) {
