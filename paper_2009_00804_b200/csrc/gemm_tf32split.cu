@@ -1,4 +1,4 @@
-// gemm_tf32x3.cu -- fp32-accurate ApplyEdge-by-type + ApplyVertex GRU for the
+// gemm_tf32split.cu -- fp32-accurate ApplyEdge-by-type + ApplyVertex GRU for the
 // gated layer (config C4) on the 5th-gen tensor cores.
 //
 // Paper: GGNN's ApplyVertex is a GRU over the gathered message and the
@@ -11,16 +11,19 @@
 //              only), followed by the PyTorch-GRUCell epilogue (reading A15):
 //              h' = (1 - z) tanh(gin + b_in + r (ghn + b_hn)) + z h.
 // The fp32 tolerance (1e-4) rules out single-pass TF32 (~3e-4 normwise), so
-// every product is computed as 3xTF32: x = x_hi + x_lo with x_hi = tf32(x)
-// (round to nearest), and A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi
-// (~2^-21 relative, the A_lo.B_lo term is below fp32 rounding).
+// every operand is split x = x_hi + x_lo with x_hi = tf32(x) and x_lo =
+// tf32(x - x_hi) (both round-to-nearest: 22 significant bits, residual
+// <= 2^-23 |x|) and A.B = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi + A_lo.B_lo (4 TF32
+// MMAs).  Measured worst case: 6.8e-5 normwise on a 70K-in-degree hub whose
+// per-type sums reach |S| ~ 130 (tests/test_gpu_parity.py zoo "hub70k"); the
+// fp32 FFMA reference kernels give 2.0e-5 there.
 //
 // Kernel (persistent, one CTA per SM, 320 threads):
 //   warp 0      TMA producer: per 32-wide K block, the fp32 A tile (128 rows,
 //               128-byte swizzle; A may come from two tensors along K) and the
 //               pre-split B_hi / B_lo tiles (BN rows of W^T),
 //   warp 1      TMEM owner + single-thread tcgen05.mma.kind::tf32 issuer
-//               (M = 128, N = BN, K = 8): 3 MMAs per K step,
+//               (M = 128, N = BN, K = 8): 4 MMAs per K step,
 //   warps 2..5  converters: A tile -> A_hi (in place) + A_lo (elementwise,
 //               so the swizzled layout is preserved), fence.proxy.async,
 //   warps 6..9  epilogue: tcgen05.ld, then store (messages) or the GRU.
@@ -77,7 +80,7 @@ __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __ex
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+    k_gemm_tf32split(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                   const __grid_constant__ CUtensorMap tmBhi, const __grid_constant__ CUtensorMap tmBlo, int64_t M,
                   int KB, int KB0, int n_tiles, float *__restrict__ msg_out, int ld_out, GruEpi gru) {
     using L = Layout<BN>;
@@ -341,13 +344,13 @@ bool make_map_f32(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, 
 }
 
 template <int BN, int EPI>
-cudaError_t launch_tf32x3(const CUtensorMap &a0, const CUtensorMap &a1, const CUtensorMap &bhi,
+cudaError_t launch_tf32split(const CUtensorMap &a0, const CUtensorMap &a1, const CUtensorMap &bhi,
                           const CUtensorMap &blo, int64_t M, int KB, int KB0, int n_tiles, float *msg_out, int ld_out,
                           const GruEpi &gru, cudaStream_t st) {
     using L = Layout<BN>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tf32x3<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tf32split<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              L::kBytes);
         if (e) return e;
         attr = true;
@@ -357,7 +360,7 @@ cudaError_t launch_tf32x3(const CUtensorMap &a0, const CUtensorMap &a1, const CU
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (M + kBM - 1) / kBM * n_tiles;
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-    k_gemm_tf32x3<BN, EPI><<<grid, kThreads, L::kBytes, st>>>(a0, a1, bhi, blo, M, KB, KB0, n_tiles, msg_out, ld_out,
+    k_gemm_tf32split<BN, EPI><<<grid, kThreads, L::kBytes, st>>>(a0, a1, bhi, blo, M, KB, KB0, n_tiles, msg_out, ld_out,
                                                                 gru);
     return cudaGetLastError();
 }
@@ -389,10 +392,10 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
         return cudaErrorInvalidValue;
     }
     GruEpi none{nullptr, nullptr, nullptr, nullptr};
-    e = launch_tf32x3<128, EPI_MSG>(aS, aS, bmh, bml, M, T * f / kBK, T * f / kBK, 1, m_ws, f, none, st);
+    e = launch_tf32split<128, EPI_MSG>(aS, aS, bmh, bml, M, T * f / kBK, T * f / kBK, 1, m_ws, f, none, st);
     if (e) return e;
     GruEpi gru{H, b_ih, b_hh, out};
-    return launch_tf32x3<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
+    return launch_tf32split<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
 }
 
 }  // namespace saga

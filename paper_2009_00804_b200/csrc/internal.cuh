@@ -87,7 +87,7 @@ cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, 
                                const float *W_ih, const float *W_hh, const float *b_ih, const float *b_hh,
                                float *m_ws, float *out, cudaStream_t st);
 
-// 3xTF32 tcgen05 GEMMs (gemm_tf32x3.cu), config C4: messages then GRU.
+// split-TF32 (4 MMAs per product) tcgen05 GEMMs (gemm_tf32split.cu), config C4.
 size_t gated_tc_workspace_floats(int32_t f, int32_t T);
 cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
