@@ -118,12 +118,13 @@ struct SumBf16Op {
 #pragma unroll
         for (int i = 0; i < NB / 2; ++i) ptx::add_bf16x2_f32(c.a[2 * i], c.a[2 * i + 1], v.w[i]);
     }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float rs, int lane) const {
+    // Ws: the bias staged in shared memory by the engine (nullptr: no bias)
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float rs, int lane, const float *Ws) const {
         uint32_t pk[NB / 2];
 #pragma unroll
         for (int h = 0; h < NB / 2; ++h) {
             float2 b = make_float2(0.f, 0.f);
-            if (bias) b = __ldg(reinterpret_cast<const float2 *>(bias + lane * NB) + h);
+            if (bias) b = reinterpret_cast<const float2 *>(Ws + lane * NB)[h];
             pk[h] = ptx::pack_bf16x2(act_fn(fmaf(rs, c.a[2 * h], b.x), kAct),
                                      act_fn(fmaf(rs, c.a[2 * h + 1], b.y), kAct));
         }
@@ -252,7 +253,7 @@ struct GatOp {
         c.a1 = fmaf(c.a1, co, cn * f.y);
         c.m = up ? s : c.m;
     }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane) const {
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
         const float inv = c.l > 0.0f ? 1.0f / c.l : 0.0f;
         float x0 = c.a0 * inv, x1 = c.a1 * inv;
         x0 = x0 > 0.0f ? x0 : expm1f(x0);
@@ -308,7 +309,7 @@ struct TypedF32Op {
                 c.a[tt][3] += (double)v.x.w;
             }
     }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane) const {
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             reinterpret_cast<float4 *>(S + ((int64_t)v * 4 + t) * 128)[lane] =
@@ -343,8 +344,8 @@ __device__ __forceinline__ auto do_finish(const Op &op, int32_t v, const typenam
 }
 template <typename Op>
 __device__ __forceinline__ void do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int lane,
-                                          const float *, long) {
-    op.finish(v, c, rs, lane);
+                                          const float *Ws, long) {
+    op.finish(v, c, rs, lane, Ws);
 }
 
 // Split rows (hubs, rows straddling a task boundary): every task holding part
@@ -379,7 +380,7 @@ struct DenseWarp {
     Val park[U][32];
     int32_t re[32];        // row_end of rows wr .. wr+31
     float rv[32 * kWinD];  // per-row values of the same rows (kWinD per row)
-    int32_t wr, v0, row_beg, head_beg, head_end, head;
+    int32_t wr, head_end;
 };
 
 template <int U, int kMinB, bool kTyped, typename Op>
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     static_assert(32 % U == 0, "U must divide the 32-edge chunk");
     using DW = DenseWarp<U, typename Op::Val, kWinD>;
     __shared__ DW warps[kWarpsPerBlock];
-    extern __shared__ float Ws[];  // ApplyVertex weight of fused-GEMV ops
+    extern __shared__ float Ws[];  // epilogue operand staged per block: fused-GEMV weight, or bias
     if (Wg) {
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
         __syncthreads();
@@ -420,14 +421,11 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         if (lane == 0) VW.wr = wbase;
         __syncwarp();
     };
-    if (lane == 0) {
-        const int32_t rb = (int32_t)g.row_ptr[v];
-        VW.v0 = v;
-        VW.row_beg = rb;
-        VW.head_beg = rb;
-        VW.head_end = -1;
-        VW.head = rb < p;  // the first row began in an earlier task
-    }
+    const int32_t v0 = v;
+    const int32_t head_beg = (int32_t)g.row_ptr[v];
+    bool head_open = head_beg < p;  // the first row began in an earlier task (its partial is pending)
+    const bool head = head_open;
+    if (lane == 0) VW.head_end = -1;
     fill_window(v);
     int32_t row_end = VW.re[0];
     float rs = kWin ? VW.rv[Op::win_col(lane)] : 0.0f;
@@ -437,19 +435,21 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
 
     // finish row v (or save its partial if it is the head row), advance to v+1
     auto flush = [&]() {
-        if (VW.head && v == VW.v0) {
+        if (head_open) {
             op.save(ws.partials + 2 * k * Op::kSlot, acc, lane);
             if (lane == 0) VW.head_end = row_end;
+            head_open = false;
         } else {
             do_finish(op, v, acc, rs, lane, Ws, 0);
         }
         ++v;
+        if (v - VW.wr == 32) {
+            __syncwarp();
+            fill_window(v);
+        }
         const int32_t wr = VW.wr;
-        __syncwarp();
-        if (lane == 0) VW.row_beg = row_end;
-        if (v - wr == 32) fill_window(wr + 32);
-        row_end = VW.re[v - VW.wr];
-        if (kWin) rs = VW.rv[(v - VW.wr) * kWinD + Op::win_col(lane)];
+        row_end = VW.re[v - wr];
+        if (kWin) rs = VW.rv[(v - wr) * kWinD + Op::win_col(lane)];
         op.zero(acc);
     };
 
@@ -509,15 +509,15 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         while (v < v1 && row_end == q + 1) flush();
     }
     while (v < v1) flush();
-    const int32_t v0 = VW.v0, row_beg = VW.row_beg;
+    const int32_t row_beg = (v == v0) ? head_beg : (v < g.n ? (int32_t)__ldg(g.row_ptr + v) : g.e);
     if (v < g.n && p1 > row_beg) {  // tail: row v continues into the next task
-        const int64_t slot = (VW.head && v == v0) ? 2 * k : 2 * k + 1;
+        const int64_t slot = (head && v == v0) ? 2 * k : 2 * k + 1;
         op.save(ws.partials + slot * Op::kSlot, acc, lane);
         ticket_merge(op, ws, g.T, v, row_beg, row_end, Ws);
     }
     const int32_t head_end = VW.head_end;
     if (head_end >= 0 && v != v0)  // the head row ended inside this task
-        ticket_merge(op, ws, g.T, v0, VW.head_beg, head_end, Ws);
+        ticket_merge(op, ws, g.T, v0, head_beg, head_end, Ws);
 }
 
 template <int U, bool kTyped, int kMinB, typename Op>
@@ -536,15 +536,15 @@ cudaError_t agg_sum_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, c
     switch (f) {
         case 256: {
             SumBf16Op<kAct, 8> op{X, scale, bias, out};
-            return run<8, false, 4>(g, op, ws, st);
+            return run<8, false, 4>(g, op, ws, st, bias, bias ? f : 0);
         }
         case 128: {
             SumBf16Op<kAct, 4> op{X, scale, bias, out};
-            return run<8, false, 4>(g, op, ws, st);
+            return run<8, false, 4>(g, op, ws, st, bias, bias ? f : 0);
         }
         case 64: {
             SumBf16Op<kAct, 2> op{X, scale, bias, out};
-            return run<8, false, 4>(g, op, ws, st);
+            return run<8, false, 4>(g, op, ws, st, bias, bias ? f : 0);
         }
     }
     return cudaErrorInvalidValue;
