@@ -116,8 +116,8 @@ def algorithmic(cfg):
     """Algorithmic (compulsory) bytes and FLOPs PER LAUNCH of each kernel
     (DESIGN.md section 5): every array the kernel must touch, once; FLOPs are
     the layer's own arithmetic counted once.  `peak` names the roofline the
-    kernel is held to: "hbm", or "tensor_bf16" / "tensor_tf32x4" (split TF32: the
-    fp32-accurate product costs four TF32 MMAs, so its peak is TF32 / 4)."""
+    kernel is held to: "hbm", or "tensor_bf16" / "tensor_tf32x3" (3xTF32: the
+    fp32-accurate product costs three TF32 MMAs, so its peak is TF32 / 3)."""
     n, e = cfg.n, cfg.num_edges
     out = {}
     if cfg.model == "gcn" and cfg.dtype == "bf16":
@@ -147,9 +147,9 @@ def algorithmic(cfg):
         out["agg_typed_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f,
                                 "peak": "hbm"}
         # S read, m written + read, h read twice (GEMM A operand, GRU epilogue), h' written
-        out["gated_apply_tf32x4"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
-                                     "peak": "tensor_tf32x4"}
-        out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x4"], peak="hbm")
+        out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
+                                     "peak": "tensor_tf32x3"}
+        out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x3"], peak="hbm")
     return out
 
 
@@ -160,12 +160,12 @@ def roofline_of(name, spec, avg_s, pk, traffic):
     if spec["peak"] == "hbm":
         ach = spec["bytes"] / avg_s / 1e9
         return dict(base, bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"])
-    # tensor: bf16 measured burst peak; TF32 = bf16 x (1.1 / 2.25 nominal ratio); split TF32 = TF32 / 4
+    # tensor: bf16 measured burst peak; TF32 = bf16 x (1.1 / 2.25 nominal ratio); 3xTF32 = TF32 / 3
     peak = pk["bf16_tflops"]
     note = "measured bf16 burst"
-    if spec["peak"] == "tensor_tf32x4":
-        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 4.0
-        note = "measured bf16 burst x nominal tf32/bf16 (1.1/2.25) / 4 (4-MMA split TF32)"
+    if spec["peak"] == "tensor_tf32x3":
+        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
+        note = "measured bf16 burst x nominal tf32/bf16 (1.1/2.25) / 3 (3xTF32)"
     # a contraction whose bytes take longer than its FLOPs is HBM-bound
     if spec["bytes"] / (pk["hbm_gbs"] * 1e9) > spec["flops"] / (peak * 1e12):
         ach = spec["bytes"] / avg_s / 1e9

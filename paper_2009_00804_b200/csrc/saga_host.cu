@@ -413,7 +413,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 return SAGA_OK;
             }
             {
-                ProfScope ps_("gated_apply_tf32x4", st);
+                ProfScope ps_("gated_apply_tf32x3", st);
                 e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data),
                                           w->W_type, w->W_ih, w->W_hh, w->b_ih, w->b_hh, m,
                                           reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);

@@ -32,7 +32,7 @@ def test_c5_aggregation_compulsory_bytes(bench):
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
 def test_every_profiled_kernel_has_a_model(bench, cfg):
     expected = {"C1": {"gcn_f32_fused"}, "C2": {"agg_mean_bf16", "gemm_bf16_tc"},
-                "C3": {"gemm_bf16_tc_gat", "gat_edge"}, "C4": {"agg_typed_f32", "gated_apply_tf32x4"},
+                "C3": {"gemm_bf16_tc_gat", "gat_edge"}, "C4": {"agg_typed_f32", "gated_apply_tf32x3"},
                 "C5": {"gemm_bf16_tc", "agg_gcn_bf16"}}[cfg]
     alg = bench.algorithmic(W.CONFIGS[cfg])
     assert expected <= set(alg)
@@ -54,8 +54,8 @@ def test_roofline_object(bench):
     r = bench.roofline_of("k", {"bytes": 6.5e9, "flops": 1, "peak": "hbm"}, 2e-3, pk, 1.0e10)
     assert r["bound"] == "hbm" and abs(r["achieved"] - 3250.0) < 1e-6 and abs(r["frac"] - 0.5) < 1e-12
     assert r["traffic"] == 1.0e10
-    t = bench.roofline_of("k", {"bytes": 1, "flops": 1e12, "peak": "tensor_tf32x4"}, 1e-2, pk, None)
-    assert t["bound"] == "tensor" and abs(t["peak"] - 1650.0 * 1.1 / 2.25 / 4) < 1e-9
+    t = bench.roofline_of("k", {"bytes": 1, "flops": 1e12, "peak": "tensor_tf32x3"}, 1e-2, pk, None)
+    assert t["bound"] == "tensor" and abs(t["peak"] - 1650.0 * 1.1 / 2.25 / 3) < 1e-9
     assert abs(t["achieved"] - 100.0) < 1e-9
 
 
@@ -65,5 +65,5 @@ def test_hbm_bound_contraction_is_held_to_hbm(bench):
     spec = bench.algorithmic(W.CONFIGS["C5"])["gemm_bf16_tc"]
     r = bench.roofline_of("gemm_bf16_tc", spec, 0.7e-3, pk, None)
     assert r["bound"] == "hbm" and r["unit"] == "GB/s"
-    c4 = bench.algorithmic(W.CONFIGS["C4"])["gated_apply_tf32x4"]
+    c4 = bench.algorithmic(W.CONFIGS["C4"])["gated_apply_tf32x3"]
     assert bench.roofline_of("g", c4, 0.36e-3, pk, None)["bound"] == "tensor"
