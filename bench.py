@@ -183,6 +183,23 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, device) -> float:
+    """Max of a per-rank scalar over all ranks (1 rank: itself).  Timing rule:
+    multi-GPU numbers are the slowest rank's device time."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(units_per_step: int, steps: int, world_size: int, max_ms: float) -> float:
+    """Whole-job throughput: the units every rank processed (weak scaling: each
+    replica does a full step) over the slowest rank's time."""
+    return units_per_step * steps * world_size / (max_ms / 1e3)
+
+
 def emit(obj, rank):
     if rank == 0:
         print(json.dumps(obj), flush=True)
@@ -329,13 +346,9 @@ def run_saga(args, cfg):
     if ws > 1:
         torch.distributed.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([tot_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = max_over_ranks(sum(step_ms), dev)
     upd_step = cfg.layer_updates()
-    value = upd_step * args.steps * ws / (tot_ms / 1e3)
+    value = job_value(upd_step, args.steps, ws, tot_ms)
     launches = sum(n for n, _ in prof.values())
 
     # roofline of the dominant kernel (largest share of the step)
@@ -416,12 +429,9 @@ def run_e2e(args, cfg, saga, H, d, dev, ws):
         if it > 0:   # first iteration is warm-up
             times.append(dt)
     d2h = out_host.numel() * out_host.element_size()
-    tmax = sum(times)
-    if ws > 1:
-        t = torch.tensor([tmax], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tmax = float(t.item())
-    return {"value": cfg.layer_updates() * len(times) * ws / tmax, "unit": UNIT, "h2d_bytes_per_step": h2d,
+    tmax = max_over_ranks(sum(times), dev)
+    return {"value": job_value(cfg.layer_updates(), len(times), ws, tmax * 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * tmax / len(times),
             "includes": "H2D COO+features, saga_graph_build, layer, D2H output"}
 
