@@ -159,7 +159,10 @@ def roofline_of(name, spec, avg_s, pk, traffic):
             "algorithmic_bytes": spec["bytes"], "algorithmic_flops": spec["flops"], "peak_source": pk["source"]}
     if spec["peak"] == "hbm":
         ach = spec["bytes"] / avg_s / 1e9
-        return dict(base, bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"])
+        r = dict(base, bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"])
+        if traffic:  # DRAM-throughput fraction: the ncu bytes this kernel really moves, at this launch time
+            r["dram_frac"] = traffic / avg_s / 1e9 / pk["hbm_gbs"]
+        return r
     # tensor: bf16 measured burst peak; TF32 = bf16 x (1.1 / 2.25 nominal ratio); 3xTF32 = TF32 / 3
     peak = pk["bf16_tflops"]
     note = "measured bf16 burst"

@@ -53,7 +53,7 @@ def test_roofline_object(bench):
     pk = {"hbm_gbs": 6500.0, "bf16_tflops": 1650.0, "bf16_tflops_sustained": 1390.0, "source": "measured"}
     r = bench.roofline_of("k", {"bytes": 6.5e9, "flops": 1, "peak": "hbm"}, 2e-3, pk, 1.0e10)
     assert r["bound"] == "hbm" and abs(r["achieved"] - 3250.0) < 1e-6 and abs(r["frac"] - 0.5) < 1e-12
-    assert r["traffic"] == 1.0e10
+    assert r["traffic"] == 1.0e10 and abs(r["dram_frac"] - 1.0e10 / 2e-3 / 6.5e12) < 1e-12
     t = bench.roofline_of("k", {"bytes": 1, "flops": 1e12, "peak": "tensor_tf32x3"}, 1e-2, pk, None)
     assert t["bound"] == "tensor" and abs(t["peak"] - 1650.0 * 1.1 / 2.25 / 3) < 1e-9
     assert abs(t["achieved"] - 100.0) < 1e-9
