@@ -51,6 +51,8 @@ def lib():
         L.oracle_gat.argtypes = [i32, P, P, P, ctypes.c_int, i32, P, i32, i32, P, P, dbl, P, i64, P, P]
         L.oracle_gated.restype = None
         L.oracle_gated.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, P, P, P, P, i64, P]
+        L.oracle_rgcn.restype = None
+        L.oracle_rgcn.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, i32, P, ctypes.c_int, P, i64, P]
         _lib = L
     return _lib
 
@@ -188,6 +190,20 @@ def gated(g: CSR, H, W_type, W_ih, W_hh, b_ih, b_hh, num_etypes=None, rows=None)
     lib().oracle_gated(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(g.etype), T, _ptr(x), xd, f,
                        _ptr(Wt), _ptr(_f64(W_ih)), _ptr(_f64(W_hh)), _ptr(_f64(b_ih)), _ptr(_f64(b_hh)),
                        _ptr(r), nr, _ptr(out))
+    return out
+
+
+def rgcn(g: CSR, H, W_type, W_self, b=None, act=1, rows=None):
+    """R-GCN layer (oracle.c oracle_rgcn; reading A24)."""
+    x, xd = _features(H)
+    Wt = _f64(W_type)
+    T, f, f_out = Wt.shape
+    Ws = _f64(W_self)
+    bb = None if b is None else _f64(b)
+    r, nr = _rows(rows, g.n)
+    out = np.zeros((nr, f_out), np.float64)
+    lib().oracle_rgcn(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(g.etype), T, _ptr(x), xd, f, _ptr(Wt),
+                      _ptr(Ws), f_out, _ptr(bb), act, _ptr(r), nr, _ptr(out))
     return out
 
 

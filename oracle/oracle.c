@@ -298,3 +298,57 @@ void oracle_gated(int32_t n, const int64_t *row_ptr, const int32_t *col_src, con
         free(S); free(m); free(h); free(gi); free(gh);
     }
 }
+
+/* ------------------------------------------------------------------------
+ * R-GCN layer.  Table 1: Scatter edge+src
+ * (the edge's relation type and the source embedding), ApplyEdge MLP (a
+ * per-type transform: "RGCN assigns another edge type attribute to
+ * different edges ... first needs to select edges with the same type and then
+ * batches them to GEMM", lines 327-328), Gather sum(in_edges) + vertex,
+ * ApplyVertex sum.  Reading A24: the relational GCN of the
+ * cited R-GCN paper with per-(destination, type) mean normalisation
+ * c_{v,t} = |N_t(v)| and a self connection W_self:
+ *   out[v] = act( sum_t (1/c_{v,t}) sum_{e=(u->v), type(e)=t} H[u] . W_t
+ *                 + H[v] . W_self + b )
+ * (a type with no in-edges of v contributes 0).  W_type [T][f][f_out],
+ * W_self [f][f_out], act 0 none / 1 ReLU.
+ * ---------------------------------------------------------------------- */
+void oracle_rgcn(int32_t n, const int64_t *row_ptr, const int32_t *col_src, const int32_t *etype_csr,
+                 int32_t num_etypes, const void *x, int x_dtype, int32_t f, const double *W_type,
+                 const double *W_self, int32_t f_out, const double *b, int act,
+                 const int64_t *rows, int64_t nrows, double *out) {
+    if (!rows) nrows = n;
+#pragma omp parallel
+    {
+        double *S = (double *)malloc(sizeof(double) * (size_t)num_etypes * (size_t)f);
+        int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (size_t)num_etypes);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < nrows; ++i) {
+            int64_t v = row_at(rows, i);
+            for (int64_t q = 0; q < (int64_t)num_etypes * f; ++q) S[q] = 0.0;
+            for (int32_t t = 0; t < num_etypes; ++t) cnt[t] = 0;
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {        /* Gather: per-type sums */
+                int32_t t = etype_csr ? etype_csr[p] : 0;
+                cnt[t] += 1;
+                for (int32_t k = 0; k < f; ++k) S[(int64_t)t * f + k] += load_x(x, x_dtype, col_src[p], f, k);
+            }
+            double *o = out + i * (int64_t)f_out;
+            for (int32_t j = 0; j < f_out; ++j) o[j] = b ? b[j] : 0.0;
+            for (int32_t t = 0; t < num_etypes; ++t) {                        /* ApplyEdge by type, mean */
+                if (cnt[t] == 0) continue;
+                for (int32_t k = 0; k < f; ++k) {
+                    double s = S[(int64_t)t * f + k] / (double)cnt[t];
+                    for (int32_t j = 0; j < f_out; ++j) o[j] += s * W_type[((int64_t)t * f + k) * f_out + j];
+                }
+            }
+            for (int32_t k = 0; k < f; ++k) {                                 /* the vertex's own term */
+                double hk = load_x(x, x_dtype, v, f, k);
+                for (int32_t j = 0; j < f_out; ++j) o[j] += hk * W_self[(int64_t)k * f_out + j];
+            }
+            if (act == 1)
+                for (int32_t j = 0; j < f_out; ++j) o[j] = o[j] > 0.0 ? o[j] : 0.0;
+        }
+        free(S);
+        free(cnt);
+    }
+}
