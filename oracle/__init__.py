@@ -185,6 +185,8 @@ def gated(g: CSR, H, W_type, W_ih, W_hh, b_ih, b_hh, num_etypes=None, rows=None)
     x, xd = _features(H)
     Wt = _f64(W_type)
     T, f, _ = Wt.shape
+    if g.etype.size and int(g.etype.max()) >= T:
+        raise ValueError(f"graph has edge types >= T = {T}")
     r, nr = _rows(rows, g.n)
     out = np.zeros((nr, f), np.float64)
     lib().oracle_gated(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(g.etype), T, _ptr(x), xd, f,
@@ -198,6 +200,8 @@ def rgcn(g: CSR, H, W_type, W_self, b=None, act=1, rows=None):
     x, xd = _features(H)
     Wt = _f64(W_type)
     T, f, f_out = Wt.shape
+    if g.etype.size and int(g.etype.max()) >= T:
+        raise ValueError(f"graph has edge types >= T = {T}")
     Ws = _f64(W_self)
     bb = None if b is None else _f64(b)
     r, nr = _rows(rows, g.n)

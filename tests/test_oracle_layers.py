@@ -284,7 +284,7 @@ def _all_models(g, n, X, et=None):
     P = [np.sin(np.arange(k)).reshape(sh) for k, sh in
          [(2 * f * f, (2, f, f)), (3 * f * f, (3, f, f)), (3 * f * f, (3, f, f)), (3 * f, (3, f)), (3 * f, (3, f))]]
     return [oracle.gcn(g, X, Wg), oracle.sage_mean(g, X, Ws), oracle.gat(g, X, Wg, a, a[::-1]),
-            oracle.gated(g, X, *P), oracle.rgcn(g, X, Wg[None], Wg[:, ::-1].copy())]
+            oracle.gated(g, X, *P), oracle.rgcn(g, X, np.stack([Wg, Wg[::-1]]), Wg[:, ::-1].copy())]
 
 
 def test_relabel_equivariance_bitexact():
