@@ -150,6 +150,14 @@ def algorithmic(cfg):
         out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
                                      "peak": "tensor_tf32x3"}
         out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x3"], peak="hbm")
+    elif cfg.model == "rgcn":
+        f, fo = cfg.dims
+        T = cfg.num_etypes
+        out["agg_typed_mean_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f,
+                                     "peak": "hbm"}
+        # S read, H read, out written
+        out["rgcn_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 + n * fo * 4, "flops": 2 * n * (T + 1) * f * fo,
+                                    "peak": "tensor_tf32x3"}
     return out
 
 
@@ -231,6 +239,8 @@ def harness_step_rows(cfg, og, c, rows, oracle):
         return oracle.sage_mean(og, h1, c["W2"].float(), act=0)
     if cfg.model == "gat":
         return oracle.gat(og, c["X"], c["W"].float(), c["a_src"], c["a_dst"], 0.2, rows=rows)
+    if cfg.model == "rgcn":
+        return oracle.rgcn(og, c["H"], c["W_type"], c["W_self"], c["b"], act=1, rows=rows)
     return oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)
 
 
@@ -291,7 +301,8 @@ def workload_config(cfg):
             "C2": "GraphSAGE-mean x2 bf16, R-MAT N=2^16 E=2^20 distinct, 128->128->64",
             "C3": "GAT 8x8 heads bf16, R-MAT N=2^18 E=2^22+self-loops, 256->64",
             "C4": "gated GRU fp32, R-MAT N=2^17 E=2^21, 4 edge types, 128",
-            "C5": "GCN at scale bf16, R-MAT N=2^22 E=2^26+self-loops, 256->256"}
+            "C5": "GCN at scale bf16, R-MAT N=2^22 E=2^26+self-loops, 256->256",
+            "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128"}
     return {"workload": f"{cfg.name}: {desc.get(cfg.name, cfg.name)}", "vertices": cfg.n, "edges": cfg.num_edges,
             "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
 

@@ -61,7 +61,8 @@ typedef enum {
     SAGA_GCN = 0,   /* Gather sum(in_edges) with D^-1/2 (A+I) D^-1/2 weights, ApplyVertex MLP  */
     SAGA_SAGE = 1,  /* Gather mean(in_edges) + vertex, ApplyVertex MLP on [x || mean]          */
     SAGA_GAT = 2,   /* ApplyEdge attention score, Gather attention(in_edges), ELU              */
-    SAGA_GATED = 3  /* per-edge-type message W_t, Gather sum(in_edges), ApplyVertex GRU        */
+    SAGA_GATED = 3, /* per-edge-type message W_t, Gather sum(in_edges), ApplyVertex GRU        */
+    SAGA_RGCN = 4   /* per-type mean messages W_t + self term, ApplyVertex sum */
 } saga_model;
 
 typedef enum { SAGA_ACT_NONE = 0, SAGA_ACT_RELU = 1, SAGA_ACT_ELU = 2 } saga_act;
@@ -88,11 +89,11 @@ typedef struct {
  * Unused members may be NULL.                                               */
 typedef struct {
     const void *W;         /* GCN [in][out]; SAGE [2*in][out] (self rows first); GAT [in][heads*hd];
-                              dtype = features dtype                                              */
+                              RGCN: W_self [in][out] fp32; dtype = features dtype                 */
     const float *bias;     /* [out] fp32, nullable (= 0)                                           */
     const float *attn_src; /* GAT [heads][hd] fp32 (applied to the source z)                      */
     const float *attn_dst; /* GAT [heads][hd] fp32 (applied to the destination z)                 */
-    const float *W_type;   /* GATED [T][f][f] fp32                                                 */
+    const float *W_type;   /* GATED, RGCN [T][f][f] fp32                                           */
     const float *W_ih;     /* GATED [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form)      */
     const float *W_hh;     /* GATED [3][f][f] fp32                                                 */
     const float *b_ih;     /* GATED [3][f] fp32                                                    */
@@ -168,6 +169,10 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *  GATED (lines 142-147, Table 1; BASELINE.json C4; A6, A15, A16):
  *        m[v] = sum_{u->v} x[u] . W_type[t(u->v)]; out[v] = GRUCell(m[v], x[v])
  *        F32, in_dim = out_dim = 128, num_etypes <= 4.
+ *  RGCN  (Table 1; A24):
+ *        out[v] = act( sum_t mean_{u->v, type t} x[u] . W_type[t] + x[v] . W + bias )
+ *        (a type with no in-edges of v contributes 0); F32, in_dim = out_dim
+ *        = 128, num_etypes <= 4, act NONE or RELU.
  *  features  [N][in_dim];  out  [N][out_dim] with the features' dtype
  *  workspace device scratch of at least saga_layer_workspace_bytes() bytes;
  *            contents on entry are ignored; it must not be shared by calls in

@@ -276,15 +276,18 @@ struct GatOp {
     }
 };
 
-// C4: per-edge-type sums of fp32 rows (4 floats per lane, 4 type slots),
-// accumulated in fp64: a 70K-edge hub summed in fp32 loses ~1e-4 of the
-// normwise output accuracy through the GRU (the fp32 configs' tolerance),
-// while FP64 adds cost nothing on this memory-bound loop.
+// C4 / R-GCN: per-edge-type sums of fp32 rows (4 floats per lane, 4 type
+// slots), accumulated in fp64: a 70K-edge hub summed in fp32 loses ~1e-4 of
+// the normwise output accuracy through the GRU (the fp32 configs'
+// tolerance), while FP64 adds cost nothing on this memory-bound loop.
+// kMean (R-GCN, reading A24) also counts the edges of each type and writes
+// the per-type means (0 for a type with no in-edges).
+template <bool kMean>
 struct TypedF32Op {
     static constexpr int kWin = 0;
-    static constexpr int kSlot = 2 * 4 * 128;  // doubles as float pairs
+    static constexpr int kSlot = 2 * (4 * 128 + (kMean ? 4 * 32 : 0));  // doubles as float pairs
     __device__ static int win_col(int) { return 0; }
-    struct Acc { double a[4][4]; };
+    struct Acc { double a[4][4]; int32_t c[kMean ? 4 : 1]; };
     struct Val { float4 x; };
     const float *H;
     float *S;  // [n][4][128]
@@ -294,6 +297,10 @@ struct TypedF32Op {
         for (int t = 0; t < 4; ++t)
 #pragma unroll
             for (int i = 0; i < 4; ++i) c.a[t][i] = 0.0;
+        if constexpr (kMean) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) c.c[t] = 0;
+        }
     }
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
         const char *p = reinterpret_cast<const char *>(H) + lane * 16 + (uint64_t)(uint32_t)u * 512u;
@@ -307,13 +314,18 @@ struct TypedF32Op {
                 c.a[tt][1] += (double)v.x.y;
                 c.a[tt][2] += (double)v.x.z;
                 c.a[tt][3] += (double)v.x.w;
+                if constexpr (kMean) c.c[tt] += 1;
             }
     }
     __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 4; ++t) {
+            double inv = 1.0;
+            if constexpr (kMean) inv = c.c[t] > 0 ? 1.0 / (double)c.c[t] : 0.0;
             reinterpret_cast<float4 *>(S + ((int64_t)v * 4 + t) * 128)[lane] =
-                make_float4((float)c.a[t][0], (float)c.a[t][1], (float)c.a[t][2], (float)c.a[t][3]);
+                make_float4((float)(c.a[t][0] * inv), (float)(c.a[t][1] * inv), (float)(c.a[t][2] * inv),
+                            (float)(c.a[t][3] * inv));
+        }
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
         double *d = reinterpret_cast<double *>(slot);
@@ -322,6 +334,10 @@ struct TypedF32Op {
 #pragma unroll
             for (int i = 0; i < 4; i += 2)
                 reinterpret_cast<double2 *>(d + t * 128 + lane * 4)[i / 2] = make_double2(c.a[t][i], c.a[t][i + 1]);
+        if constexpr (kMean) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) d[512 + lane * 4 + t] = (double)c.c[t];
+        }
     }
     __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
         const double *d = reinterpret_cast<const double *>(slot);
@@ -333,6 +349,10 @@ struct TypedF32Op {
                 c.a[t][i] += x.x;
                 c.a[t][i + 1] += x.y;
             }
+        if constexpr (kMean) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) c.c[t] += (int32_t)__ldcg(d + 512 + lane * 4 + t);
+        }
     }
 };
 
@@ -566,6 +586,7 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
         case SAGA_SAGE: return (size_t)(width > 32 ? width : 32);
         case SAGA_GAT: return 128;                                // 32 lanes x (m, l, a0, a1)
         case SAGA_GATED: return (size_t)2 * 4 * 128;              // 4 type slots x 128 fp64
+        case SAGA_RGCN: return (size_t)2 * (4 * 128 + 4 * 32);    // + per-type edge counts
     }
     return 0;
 }
@@ -598,12 +619,17 @@ cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const flo
     return run<8, false, 4>(g, op, ws, st);
 }
 
-cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, AggWorkspace ws,
+cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,
                                  cudaStream_t st) {
     if (f != 128) return cudaErrorInvalidValue;
-    TypedF32Op op{H, S};
     // fp64 accumulators leave room for U = 4 at 64 registers (32 warps/SM),
     // measured faster than U = 8 at 2-3 blocks/SM
+    if (mean) {
+        TypedF32Op<true> op{H, S};
+        if (g.etype) return run<4, true, 4>(g, op, ws, st);
+        return run<4, false, 4>(g, op, ws, st);
+    }
+    TypedF32Op<false> op{H, S};
     if (g.etype) return run<4, true, 4>(g, op, ws, st);
     return run<4, false, 4>(g, op, ws, st);
 }

@@ -69,6 +69,8 @@ struct GruEpi {
     const float *b_ih;   // [3][128]
     const float *b_hh;   // [3][128]
     float *out;          // [M][128]
+    const float *bias;   // EPI_MSG: optional bias [N]
+    int relu;            // EPI_MSG: ReLU
 };
 
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -217,11 +219,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_ld32(tbase + c * 32, v);
                     ptx::tmem_ld_wait();
                     if (row < M) {
-                        float4 *o = reinterpret_cast<float4 *>(msg_out + row * ld_out + nt * BN + c * 32);
+                        const int col0 = nt * BN + c * 32;
+                        float x[32];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                        for (int j = 0; j < 32; ++j) {
+                            x[j] = __uint_as_float(v[j]) + (gru.bias ? __ldg(gru.bias + col0 + j) : 0.0f);
+                            if (gru.relu) x[j] = fmaxf(x[j], 0.0f);
+                        }
+                        float4 *o = reinterpret_cast<float4 *>(msg_out + row * ld_out + col0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
                     }
                 }
             } else {
@@ -312,6 +319,20 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
     }
 }
 
+// R-GCN B^T in K-major layout, split hi/lo: Br[n][k], k < T f from W_type[k / f][k % f][n],
+// k >= T f from W_self[k - T f][n]  (N = f_out = f, K = (T + 1) f).
+__global__ void k_split_rgcn(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_self,
+                             float *b_hi, float *b_lo) {
+    const int K = (T + 1) * f, total = f * K;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int n = i / K, k = i % K;
+        const float x = k < T * f ? W_type[((int64_t)(k / f) * f + k % f) * f + n] : W_self[(int64_t)(k - T * f) * f + n];
+        const float h = tf32_rna(x);
+        b_hi[i] = h;
+        b_lo[i] = tf32_rna(x - h);
+    }
+}
+
 // ------------------------------------------------------------- host side ----
 using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                               const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -367,6 +388,31 @@ cudaError_t launch_tf32split(const CUtensorMap &a0, const CUtensorMap &a1, const
 
 }  // namespace
 
+size_t rgcn_tc_workspace_floats(int32_t f, int32_t T) { return (size_t)2 * f * (T + 1) * f; }
+
+cudaError_t launch_rgcn_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H, const float *W_type,
+                                 const float *W_self, const float *bias, int act, float *wsplit, float *out,
+                                 cudaStream_t st, const char **why) {
+    if (M == 0) return cudaSuccess;
+    if (f != 128 || T < 1 || T > 4) {
+        *why = "tensor-core R-GCN path needs f = 128, 1 <= T <= 4";
+        return cudaErrorInvalidValue;
+    }
+    const int K = (T + 1) * f;
+    float *b_hi = wsplit, *b_lo = wsplit + (size_t)f * K;
+    k_split_rgcn<<<256, 256, 0, st>>>(f, T, W_type, W_self, b_hi, b_lo);
+    cudaError_t e = cudaGetLastError();
+    if (e) return e;
+    CUtensorMap aS, aH, bh, bl;
+    if (!make_map_f32(&aS, S, M, (int64_t)T * f, 4 * f, kBM) || !make_map_f32(&aH, H, M, f, f, kBM) ||
+        !make_map_f32(&bh, b_hi, f, K, K, 128) || !make_map_f32(&bl, b_lo, f, K, K, 128)) {
+        *why = "cuTensorMapEncodeTiled failed";
+        return cudaErrorInvalidValue;
+    }
+    GruEpi epi{nullptr, nullptr, nullptr, nullptr, bias, act == SAGA_ACT_RELU};
+    return launch_tf32split<128, EPI_MSG>(aS, aH, bh, bl, M, K / kBK, T * f / kBK, 1, out, f, epi, st);
+}
+
 size_t gated_tc_workspace_floats(int32_t f, int32_t T) { return (size_t)2 * f * T * f + (size_t)2 * 4 * f * 2 * f; }
 
 cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
@@ -391,10 +437,10 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
         *why = "cuTensorMapEncodeTiled failed";
         return cudaErrorInvalidValue;
     }
-    GruEpi none{nullptr, nullptr, nullptr, nullptr};
+    GruEpi none{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
     e = launch_tf32split<128, EPI_MSG>(aS, aS, bmh, bml, M, T * f / kBK, T * f / kBK, 1, m_ws, f, none, st);
     if (e) return e;
-    GruEpi gru{H, b_ih, b_hh, out};
+    GruEpi gru{H, b_ih, b_hh, out, nullptr, 0};
     return launch_tf32split<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
 }
 

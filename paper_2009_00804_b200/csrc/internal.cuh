@@ -61,7 +61,8 @@ cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int3
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
 // GATED typed sums: S[v][t][:] = sum_{type t} H[u]  (fp32)
-cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, AggWorkspace ws,
+// GATED / RGCN typed sums (mean = per-type means, R-GCN): S[v][t][:]  (fp32, fp64 accumulation)
+cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,
                                  cudaStream_t st);
 
 // ----------------------------------------------------------------- GEMM ----
@@ -93,5 +94,11 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
                                   const float *b_hh, float *m_ws, float *wsplit, float *out, cudaStream_t st,
                                   const char **why);
+
+// R-GCN ApplyVertex (NEXT-3): out = act([S_0..S_{T-1} || H] . [W_0; ..; W_{T-1}; W_self] + b), 3xTF32.
+size_t rgcn_tc_workspace_floats(int32_t f, int32_t T);
+cudaError_t launch_rgcn_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H, const float *W_type,
+                                 const float *W_self, const float *bias, int act, float *wsplit, float *out,
+                                 cudaStream_t st, const char **why);
 
 }  // namespace saga

@@ -127,6 +127,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_SAGE: width = (size_t)o.in_dim; break;
         case SAGA_GAT: width = (size_t)o.out_dim; break;
         case SAGA_GATED: width = (size_t)o.in_dim; break;
+        case SAGA_RGCN: width = (size_t)o.in_dim; break;
     }
     size_t pf = saga::agg_partial_floats(kind, (int32_t)width, 8);
     if (kind == SAGA_GCN) pf = (size_t)2 * std::max({o.in_dim, o.out_dim, 32});  // fp64 partials on the fp32 path
@@ -145,6 +146,10 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
             p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S
             p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
             p.inter2 = align_up(sizeof(float) * saga::gated_tc_workspace_floats(128, 4));       // split W
+            break;
+        case SAGA_RGCN:
+            p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S (type means)
+            p.inter2 = align_up(sizeof(float) * saga::rgcn_tc_workspace_floats(128, 4));        // split W
             break;
     }
     p.total = p.counters + p.partials + p.inter0 + p.inter1 + p.inter2;
@@ -225,7 +230,7 @@ saga_status saga_graph_copy_csr(const saga_graph *g, int64_t *row_ptr, int32_t *
 saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g, const saga_layer_opts *opts,
                                        size_t *bytes) {
     if (!g || !opts || !bytes) return fail(SAGA_EINVAL, "NULL argument");
-    if (kind < SAGA_GCN || kind > SAGA_GATED) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+    if (kind < SAGA_GCN || kind > SAGA_RGCN) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
     *bytes = plan_for(kind, g->d, *opts).total;
     return SAGA_OK;
 }
@@ -402,7 +407,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             float *S = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
             {
                 ProfScope ps_("agg_typed_f32", st);
-                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, aw, st);
+                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, false, aw, st);
             }
             if (e) return cuda_fail(e, "typed aggregate");
             if (getenv("SAGA_GATED_SIMT")) {  // development knob: the FFMA reference kernels
@@ -419,6 +424,27 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                                           reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "gated apply: %s (%s)", cudaGetErrorString(e), why);
+            return SAGA_OK;
+        }
+        case SAGA_RGCN: {
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "RGCN supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "RGCN supports in=out=128");
+            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "RGCN supports <= 4 edge types");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "RGCN act must be NONE/RELU");
+            if (!w->W_type || !w->W) return fail(SAGA_EINVAL, "RGCN needs W_type and W (self)");
+            float *S = reinterpret_cast<float *>(i0);
+            {
+                ProfScope ps_("agg_typed_mean_f32", st);
+                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, true, aw, st);
+            }
+            if (e) return cuda_fail(e, "rgcn typed aggregate");
+            {
+                ProfScope ps_("rgcn_apply_tf32x3", st);
+                e = launch_rgcn_apply_tc(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
+                                         static_cast<const float *>(w->W), w->bias, o.act,
+                                         reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "rgcn apply: %s (%s)", cudaGetErrorString(e), why);
             return SAGA_OK;
         }
     }

@@ -44,6 +44,10 @@ def gpu_step(saga, cfg, g, d, layers=None):
         lay = layers[0] if layers else saga.Layer("gated", g, f, f, saga.SAGA_ACT_NONE, dt)
         w = {k: d[k].contiguous() for k in ("W_type", "W_ih", "W_hh", "b_ih", "b_hh")}
         return [lay(d["H"], w)], [lay]
+    if cfg.model == "rgcn":
+        f, fo = cfg.dims
+        lay = layers[0] if layers else saga.Layer("rgcn", g, f, fo, act_relu, dt)
+        return [lay(d["H"], {"W_type": d["W_type"].contiguous(), "W": d["W_self"], "bias": d["b"]})], [lay]
     raise ValueError(cfg.model)
 
 
@@ -70,6 +74,8 @@ def oracle_step(oracle, cfg, og, d, rows=None, layer_inputs=None):
         return [oracle.gat(og, c["X"], c["W"].float(), c["a_src"], c["a_dst"], 0.2, rows=rows)]
     if cfg.model == "gated":
         return [oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)]
+    if cfg.model == "rgcn":
+        return [oracle.rgcn(og, c["H"], c["W_type"], c["W_self"], c["b"], act=1, rows=rows)]
     raise ValueError(cfg.model)
 
 

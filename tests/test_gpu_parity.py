@@ -96,6 +96,10 @@ def _zoo_inputs(model, n, s, d, seed):
         u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
         return {"H": r(n, 128), "W_type": u(4, 128, 128), "W_ih": u(3, 128, 128), "W_hh": u(3, 128, 128),
                 "b_ih": u(3, 128), "b_hh": u(3, 128)}
+    if model == "rgcn":
+        b = 1 / np.sqrt(128)
+        u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
+        return {"H": r(n, 128), "W_type": u(4, 128, 128), "W_self": u(128, 128), "b": u(128)}
 
 
 def _zoo_cfg(model, n, e):
@@ -103,12 +107,13 @@ def _zoo_cfg(model, n, e):
             "gcn_f32": W.Config("z", "gcn", "er", n, e, False, False, "f32", (64, 16)),
             "sage": W.Config("z", "sage", "er", n, e, False, False, "bf16", (128, 128, 64)),
             "gat": W.Config("z", "gat", "er", n, e, False, False, "bf16", (256, 64), heads=8),
-            "gated": W.Config("z", "gated", "er", n, e, False, False, "f32", (128, 128), num_etypes=4)}
+            "gated": W.Config("z", "gated", "er", n, e, False, False, "f32", (128, 128), num_etypes=4),
+            "rgcn": W.Config("z", "rgcn", "er", n, e, False, False, "f32", (128, 128), num_etypes=4)}
     return base[model]
 
 
 ZOO = [z for z in zoo.zoo(include_big=True) if z[1] > 0]
-MODELS = ["gcn_bf16", "gcn_f32", "sage", "gat", "gated"]
+MODELS = ["gcn_bf16", "gcn_f32", "sage", "gat", "gated", "rgcn"]
 
 
 @pytest.mark.parametrize("model", MODELS)
@@ -120,7 +125,7 @@ def test_layer_zoo(saga, model, name, n, s, d, loops):
     cfg = _zoo_cfg(model, n, s.shape[0])
     x = _zoo_inputs(model, n, s, d, 7)
     x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
-    if model == "gated":
+    if model in ("gated", "rgcn"):
         x["etype"] = torch.from_numpy((np.arange(s.shape[0]) * 7 % 4).astype(np.int32))
     dx = H.dev_inputs(x, DEV)
     g = H.gpu_graph(saga, cfg, dx)
@@ -159,12 +164,12 @@ def _config_check(saga, cfg, rows_k=None):
         assert oracle.rel_err(yy, ref_e2e) <= tol
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6"])
 def test_config_full(saga, cfg):
     _config_check(saga, W.CONFIGS[cfg])
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6"])
 def test_config_scaled_ragged(saga, cfg):
     """Same recipe at a size that is not a multiple of any tile (ragged tails)."""
     c = W.CONFIGS[cfg]

@@ -51,7 +51,7 @@ class Config:
     def f_canon(self) -> int:
         """Row width Gather reduces in SAGA order (reading A20)."""
         return {"gcn": self.dims[0], "sage": self.dims[0], "gat": self.dims[-1],
-                "gated": self.dims[0]}[self.model]
+                "gated": self.dims[0], "rgcn": self.dims[0]}[self.model]
 
     def updates_per_layer(self) -> int:
         """Edge-feature updates of one layer = E * F_canon (reading A20).
@@ -79,6 +79,9 @@ CONFIGS = {
     "C4": Config("C4", "gated", "rmat", 1 << 17, 1 << 21, False, False, "f32", (128, 128), num_etypes=4, index=4),
     # BJ:11 GCN at scale, R-MAT 2^22, 2^26 edges + self-loops, 256 -> 256 (bf16)
     "C5": Config("C5", "gcn", "rmat", 1 << 22, 1 << 26, True, False, "bf16", (256, 256), index=5),
+    # SURVEY 8(f) NEXT-3 (not a BASELINE config): R-GCN, C4's graph shape and widths,
+    # 4 relation types, fp32, per-type mean + self connection + bias, ReLU
+    "C6": Config("C6", "rgcn", "rmat", 1 << 17, 1 << 21, False, False, "f32", (128, 128), num_etypes=4, index=6),
 }
 
 
@@ -325,6 +328,14 @@ def make_inputs(cfg: Config, device="cpu", graph=True):
         d["W_hh"] = uniform(k, "W_hh", 3 * hdim, hdim, bnd, device).view(3, hdim, hdim)
         d["b_ih"] = uniform(k, "b_ih", 3, hdim, bnd, device)
         d["b_hh"] = uniform(k, "b_hh", 3, hdim, bnd, device)
+    elif cfg.model == "rgcn":
+        f, fo = cfg.dims
+        T = cfg.num_etypes
+        bnd = 1.0 / math.sqrt(f)
+        d["H"] = normal(k, f"H/{n}", n, f, 1.0, device)
+        d["W_type"] = uniform(k, "W_type", T * f, fo, bnd, device).view(T, f, fo)
+        d["W_self"] = uniform(k, "W_self", f, fo, bnd, device)
+        d["b"] = uniform(k, "b", 1, fo, bnd, device).view(fo)
     else:
         raise ValueError(cfg.model)
     return d
