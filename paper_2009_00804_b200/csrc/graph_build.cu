@@ -363,7 +363,6 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     // (larger tasks amortise the per-task prologue and split-row tickets)
     int64_t items = e + (int64_t)n;
     int64_t target = (int64_t)kNumSMs * 64;
-    if (const char *env = getenv("SAGA_TASK_TARGET")) target = atoll(env);  // development knob
     int64_t T = std::max<int64_t>(8, (items + target - 1) / target);
     g->task_items = T;
     g->ntasks = items > 0 ? (items + T - 1) / T : 0;

@@ -1,3 +1,5 @@
+# Worst-case fp32 accuracy probe: the 70K-in-degree hub of the test zoo, gated model,
+# tensor-core path vs the FFMA reference kernels (SAGA_GATED_SIMT=1).
 cat > /tmp/hub.py <<'PY'
 import torch, numpy as np, sys, os
 sys.path.insert(0, '.')

@@ -1,1 +1,2 @@
+# The GPU parity suite only.
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15
