@@ -51,6 +51,8 @@ def lib():
         L.oracle_gat.argtypes = [i32, P, P, P, ctypes.c_int, i32, P, i32, i32, P, P, dbl, P, i64, P, P]
         L.oracle_gated.restype = None
         L.oracle_gated.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, P, P, P, P, i64, P]
+        L.oracle_sage_lstm.restype = None
+        L.oracle_sage_lstm.argtypes = [i32, P, P, P, ctypes.c_int, i32, P, P, P, P, P, i32, P, ctypes.c_int, P, i64, P]
         L.oracle_rgcn.restype = None
         L.oracle_rgcn.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, i32, P, ctypes.c_int, P, i64, P]
         _lib = L
@@ -208,6 +210,22 @@ def rgcn(g: CSR, H, W_type, W_self, b=None, act=1, rows=None):
     out = np.zeros((nr, f_out), np.float64)
     lib().oracle_rgcn(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(g.etype), T, _ptr(x), xd, f, _ptr(Wt),
                       _ptr(Ws), f_out, _ptr(bb), act, _ptr(r), nr, _ptr(out))
+    return out
+
+
+def sage_lstm(g: CSR, X, W_ih, W_hh, b_ih, b_hh, W, b=None, act=1, rows=None):
+    """GraphSAGE-LSTM layer (oracle.c oracle_sage_lstm; reading A25)."""
+    x, xd = _features(X)
+    Wi, Wh = _f64(W_ih), _f64(W_hh)
+    f = Wi.shape[1]
+    Wm = _f64(W)
+    f_out = Wm.shape[1]
+    assert Wi.shape == (4, f, f) and Wh.shape == (4, f, f) and Wm.shape[0] == 2 * f
+    bb = None if b is None else _f64(b)
+    r, nr = _rows(rows, g.n)
+    out = np.zeros((nr, f_out), np.float64)
+    lib().oracle_sage_lstm(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(x), xd, f, _ptr(Wi), _ptr(Wh),
+                           _ptr(_f64(b_ih)), _ptr(_f64(b_hh)), _ptr(Wm), f_out, _ptr(bb), act, _ptr(r), nr, _ptr(out))
     return out
 
 

@@ -352,3 +352,66 @@ void oracle_rgcn(int32_t n, const int64_t *row_ptr, const int32_t *col_src, cons
         free(cnt);
     }
 }
+
+/* ------------------------------------------------------------------------
+ * GraphSAGE-LSTM layer.  Table 1: Gather
+ * LSTM(in_edges) + vertex, ApplyVertex MLP; lines 357-360: the LSTM "treats
+ * the inedges of a vertex as a sequence and outputs a new vector".
+ * Reading A25: the sequence is v's in-edges in CSR order
+ * (ascending COO index, reading A7), the cell is the
+ * PyTorch LSTMCell (gates i, f, g, o; zero initial h, c), the gathered
+ * vector is the final h (0 for a vertex without in-edges), and ApplyVertex
+ * is the GraphSAGE concat-GEMM of reading A11:
+ *   for the in-edges u_1..u_d of v:  z = x[u_s] . W_ih + b_ih + h . W_hh + b_hh
+ *     i = s(z_i), f = s(z_f), g = tanh(z_g), o = s(z_o)
+ *     c = f * c + i * g,  h = o * tanh(c)
+ *   out[v] = act([x[v] || h] . W + b)
+ * W_ih [4][f][f], W_hh [4][f][f], b_ih/b_hh [4][f] (gate order i, f, g, o),
+ * W [2f][f_out]; act 0 none / 1 ReLU.
+ * ---------------------------------------------------------------------- */
+void oracle_sage_lstm(int32_t n, const int64_t *row_ptr, const int32_t *col_src, const void *x, int x_dtype,
+                      int32_t f, const double *W_ih, const double *W_hh, const double *b_ih, const double *b_hh,
+                      const double *W, int32_t f_out, const double *b, int act,
+                      const int64_t *rows, int64_t nrows, double *out) {
+    if (!rows) nrows = n;
+#pragma omp parallel
+    {
+        double *h = (double *)malloc(sizeof(double) * (size_t)f);
+        double *c = (double *)malloc(sizeof(double) * (size_t)f);
+        double *z = (double *)malloc(sizeof(double) * 4 * (size_t)f);
+        double *hn = (double *)malloc(sizeof(double) * (size_t)f);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < nrows; ++i) {
+            int64_t v = row_at(rows, i);
+            for (int32_t k = 0; k < f; ++k) { h[k] = 0.0; c[k] = 0.0; }
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {          /* the in-edge sequence */
+                int32_t u = col_src[p];
+                for (int32_t g = 0; g < 4; ++g)
+                    for (int32_t j = 0; j < f; ++j) z[g * f + j] = b_ih[g * f + j] + b_hh[g * f + j];
+                for (int32_t g = 0; g < 4; ++g)
+                    for (int32_t k = 0; k < f; ++k) {
+                        double xk = load_x(x, x_dtype, u, f, k), hk = h[k];
+                        for (int32_t j = 0; j < f; ++j)
+                            z[g * f + j] += xk * W_ih[((int64_t)g * f + k) * f + j] + hk * W_hh[((int64_t)g * f + k) * f + j];
+                    }
+                for (int32_t j = 0; j < f; ++j) {
+                    double ig = sigmoid(z[j]), fg = sigmoid(z[f + j]), gg = tanh(z[2 * f + j]),
+                           og = sigmoid(z[3 * f + j]);
+                    c[j] = fg * c[j] + ig * gg;
+                    hn[j] = og * tanh(c[j]);
+                }
+                for (int32_t j = 0; j < f; ++j) h[j] = hn[j];
+            }
+            double *o = out + i * (int64_t)f_out;                              /* ApplyVertex: [x || h] . W */
+            for (int32_t j = 0; j < f_out; ++j) o[j] = b ? b[j] : 0.0;
+            for (int32_t k = 0; k < f; ++k) {
+                double xk = load_x(x, x_dtype, v, f, k);
+                for (int32_t j = 0; j < f_out; ++j)
+                    o[j] += xk * W[(int64_t)k * f_out + j] + h[k] * W[(int64_t)(f + k) * f_out + j];
+            }
+            if (act == 1)
+                for (int32_t j = 0; j < f_out; ++j) o[j] = o[j] > 0.0 ? o[j] : 0.0;
+        }
+        free(h); free(c); free(z); free(hn);
+    }
+}
