@@ -150,6 +150,14 @@ def algorithmic(cfg):
         out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
                                      "peak": "tensor_tf32x3"}
         out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x3"], peak="hbm")
+    elif cfg.model == "sage_lstm":
+        f, fo = cfg.dims
+        # per edge: gather a 1 KB row of P (4 gates bf16); recurrent GEMV 2 * 4f * f FLOPs
+        out["lstm_gather"] = {"bytes": e * 4 + (n + 1) * 8 + e * 4 * f * 2 + n * f * 2 + 4 * f * f * 2,
+                              "flops": e * 2 * 4 * f * f, "peak": "hbm"}
+        out["lstm_input_gemm"] = {"bytes": n * f * 2 + f * f * 2 + n * f * 2, "flops": 2 * n * f * f,
+                                  "peak": "tensor_bf16"}
+        out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f + fo), "flops": 2 * n * 2 * f * fo, "peak": "tensor_bf16"}
     elif cfg.model == "rgcn":
         f, fo = cfg.dims
         T = cfg.num_etypes
@@ -241,6 +249,9 @@ def harness_step_rows(cfg, og, c, rows, oracle):
         return oracle.gat(og, c["X"], c["W"].float(), c["a_src"], c["a_dst"], 0.2, rows=rows)
     if cfg.model == "rgcn":
         return oracle.rgcn(og, c["H"], c["W_type"], c["W_self"], c["b"], act=1, rows=rows)
+    if cfg.model == "sage_lstm":
+        return oracle.sage_lstm(og, c["X"], c["W_ih"].float(), c["W_hh"].float(), c["b_ih"], c["b_hh"],
+                                c["W"].float(), c["b"], act=1, rows=rows)
     return oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)
 
 
@@ -302,7 +313,8 @@ def workload_config(cfg):
             "C3": "GAT 8x8 heads bf16, R-MAT N=2^18 E=2^22+self-loops, 256->64",
             "C4": "gated GRU fp32, R-MAT N=2^17 E=2^21, 4 edge types, 128",
             "C5": "GCN at scale bf16, R-MAT N=2^22 E=2^26+self-loops, 256->256",
-            "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128"}
+            "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128",
+            "C7": "GraphSAGE-LSTM bf16 (NEXT-2), R-MAT N=2^16 E=2^20 distinct, 128->128"}
     return {"workload": f"{cfg.name}: {desc.get(cfg.name, cfg.name)}", "vertices": cfg.n, "edges": cfg.num_edges,
             "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
 

@@ -62,7 +62,8 @@ typedef enum {
     SAGA_SAGE = 1,  /* Gather mean(in_edges) + vertex, ApplyVertex MLP on [x || mean]          */
     SAGA_GAT = 2,   /* ApplyEdge attention score, Gather attention(in_edges), ELU              */
     SAGA_GATED = 3, /* per-edge-type message W_t, Gather sum(in_edges), ApplyVertex GRU        */
-    SAGA_RGCN = 4   /* per-type mean messages W_t + self term, ApplyVertex sum */
+    SAGA_RGCN = 4,  /* per-type mean messages W_t + self term, ApplyVertex sum */
+    SAGA_SAGE_LSTM = 5 /* Gather LSTM(in_edges) + vertex, ApplyVertex MLP     */
 } saga_model;
 
 typedef enum { SAGA_ACT_NONE = 0, SAGA_ACT_RELU = 1, SAGA_ACT_ELU = 2 } saga_act;
@@ -94,10 +95,11 @@ typedef struct {
     const float *attn_src; /* GAT [heads][hd] fp32 (applied to the source z)                      */
     const float *attn_dst; /* GAT [heads][hd] fp32 (applied to the destination z)                 */
     const float *W_type;   /* GATED, RGCN [T][f][f] fp32                                           */
-    const float *W_ih;     /* GATED [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form)      */
-    const float *W_hh;     /* GATED [3][f][f] fp32                                                 */
-    const float *b_ih;     /* GATED [3][f] fp32                                                    */
-    const float *b_hh;     /* GATED [3][f] fp32                                                    */
+    const void *W_ih;      /* GATED [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form);
+                              SAGE_LSTM [4][f][f] bf16, gate order i, f, g, o (LSTMCell form)    */
+    const void *W_hh;      /* GATED [3][f][f] fp32; SAGE_LSTM [4][f][f] bf16                     */
+    const float *b_ih;     /* GATED [3][f], SAGE_LSTM [4][f] fp32                                  */
+    const float *b_hh;     /* GATED [3][f], SAGE_LSTM [4][f] fp32                                  */
 } saga_weights;
 
 /* Returns SAGA_ABI_VERSION. */
@@ -169,6 +171,11 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *  GATED (lines 142-147, Table 1; BASELINE.json C4; A6, A15, A16):
  *        m[v] = sum_{u->v} x[u] . W_type[t(u->v)]; out[v] = GRUCell(m[v], x[v])
  *        F32, in_dim = out_dim = 128, num_etypes <= 4.
+ *  SAGE_LSTM (Table 1; A25):
+ *        h[v] = final state of LSTMCell(W_ih, W_hh, b_ih, b_hh) run over x[u]
+ *        for v's in-edges u -> v in CSR order from a zero state (0 without
+ *        in-edges); out[v] = act([x[v] || h[v]] . W + bias), W [2*in][out]
+ *        BF16, in_dim = 128, out_dim in {64, 128, 256}, act NONE or RELU.
  *  RGCN  (Table 1; A24):
  *        out[v] = act( sum_t mean_{u->v, type t} x[u] . W_type[t] + x[v] . W + bias )
  *        (a type with no in-edges of v contributes 0); F32, in_dim = out_dim

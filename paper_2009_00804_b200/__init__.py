@@ -23,9 +23,10 @@ LIB_PATH = os.path.join(_HERE, "libsaga.so")
 SAGA_OK, SAGA_EINVAL, SAGA_ERANGE, SAGA_ESHAPE, SAGA_EDTYPE, SAGA_ENOMEM, SAGA_ECUDA, SAGA_EUNSUPPORTED, \
     SAGA_EINTERNAL = range(9)
 SAGA_F32, SAGA_BF16 = 0, 1
-SAGA_GCN, SAGA_SAGE, SAGA_GAT, SAGA_GATED, SAGA_RGCN = 0, 1, 2, 3, 4
+SAGA_GCN, SAGA_SAGE, SAGA_GAT, SAGA_GATED, SAGA_RGCN, SAGA_SAGE_LSTM = 0, 1, 2, 3, 4, 5
 SAGA_ACT_NONE, SAGA_ACT_RELU, SAGA_ACT_ELU = 0, 1, 2
-MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GATED, "rgcn": SAGA_RGCN}
+MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GATED, "rgcn": SAGA_RGCN,
+          "sage_lstm": SAGA_SAGE_LSTM}
 
 # Every symbol include/saga.h declares (checked by tests/test_abi.py).
 EXPORTS = ["saga_abi_version", "saga_graph_build", "saga_graph_info", "saga_graph_copy_csr",

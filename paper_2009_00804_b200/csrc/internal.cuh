@@ -24,6 +24,7 @@ struct GraphDev {
     int32_t *out_deg = nullptr;   // [n]
     float *dinv = nullptr;        // [n]  in_deg^-1/2 (0 if 0)  -- S1, GCN
     float *inv_deg = nullptr;     // [n]  1/in_deg (0 if 0)     -- S1, SAGE
+    int32_t *deg_order = nullptr; // [n]  vertices by in-degree, descending (LSTM work queue)
     // Merge-path load-balance schedule (S6): items = E edges + N row ends,
     // task k covers items [k*T, min((k+1)T, E+N)); its start coordinate is
     // (task_v[k], task_p[k]).  Arrays have ntasks+1 entries.
@@ -94,6 +95,12 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
                                   const float *b_hh, float *m_ws, float *wsplit, float *out, cudaStream_t st,
                                   const char **why);
+
+// GraphSAGE-LSTM Gather (lstm_gather.cu, NEXT-2): h_out[v] = final LSTM state over v's in-edges.
+size_t lstm_workspace_bytes();  // staged W_hh^T
+cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const __nv_bfloat16 *W_hh,
+                               const float *b_ih, const float *b_hh, __nv_bfloat16 *h_out, int32_t *queue,
+                               void *wt_ws, cudaStream_t st);
 
 // R-GCN ApplyVertex (NEXT-3): out = act([S_0..S_{T-1} || H] . [W_0; ..; W_{T-1}; W_self] + b), 3xTF32.
 size_t rgcn_tc_workspace_floats(int32_t f, int32_t T);

@@ -225,6 +225,15 @@ __device__ __forceinline__ void stg_v4_stream(void *p, uint4 v) {
         : "memory");
 }
 
+// acc += w.lo * h.lo + w.hi * h.hi with bf16 x bf16 products in fp32
+// (sm_100 mixed-precision FMA: two FHFMA.BF16, no unpacking).
+__device__ __forceinline__ void fma_bf16x2_f32(float &acc, uint32_t w, uint32_t h) {
+    asm("{\n.reg .b16 wl, wh, hl, hh;\nmov.b32 {wl, wh}, %1;\nmov.b32 {hl, hh}, %2;\n"
+        "fma.rn.f32.bf16 %0, wl, hl, %0;\nfma.rn.f32.bf16 %0, wh, hh, %0;\n}"
+        : "+f"(acc)
+        : "r"(w), "r"(h));
+}
+
 // 2^x on the SFU, flush-to-zero (one MUFU.EX2, no range fix-up).
 __device__ __forceinline__ float exp2_ftz(float x) {
     float y;

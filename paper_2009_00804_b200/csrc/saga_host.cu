@@ -128,6 +128,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GAT: width = (size_t)o.out_dim; break;
         case SAGA_GATED: width = (size_t)o.in_dim; break;
         case SAGA_RGCN: width = (size_t)o.in_dim; break;
+        case SAGA_SAGE_LSTM: width = (size_t)o.in_dim; break;
     }
     size_t pf = saga::agg_partial_floats(kind, (int32_t)width, 8);
     if (kind == SAGA_GCN) pf = (size_t)2 * std::max({o.in_dim, o.out_dim, 32});  // fp64 partials on the fp32 path
@@ -146,6 +147,11 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
             p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S
             p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
             p.inter2 = align_up(sizeof(float) * saga::gated_tc_workspace_floats(128, 4));       // split W
+            break;
+        case SAGA_SAGE_LSTM:
+            p.inter0 = align_up((size_t)2 * 4 * n * (size_t)std::max(o.in_dim, 0));             // P = X W_ih, bf16
+            p.inter1 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0));                 // h (LSTM out), bf16
+            p.inter2 = align_up(saga::lstm_workspace_bytes());                                  // staged W_hh^T
             break;
         case SAGA_RGCN:
             p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S (type means)
@@ -230,7 +236,7 @@ saga_status saga_graph_copy_csr(const saga_graph *g, int64_t *row_ptr, int32_t *
 saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g, const saga_layer_opts *opts,
                                        size_t *bytes) {
     if (!g || !opts || !bytes) return fail(SAGA_EINVAL, "NULL argument");
-    if (kind < SAGA_GCN || kind > SAGA_RGCN) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+    if (kind < SAGA_GCN || kind > SAGA_SAGE_LSTM) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
     *bytes = plan_for(kind, g->d, *opts).total;
     return SAGA_OK;
 }
@@ -413,17 +419,65 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (getenv("SAGA_GATED_SIMT")) {  // development knob: the FFMA reference kernels
                 ProfScope ps_("gated_apply_sgemm", st);
                 e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
-                                   w->W_ih, w->W_hh, w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
+                                       static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
+                                       w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
                 if (e) return cuda_fail(e, "gated apply");
                 return SAGA_OK;
             }
             {
                 ProfScope ps_("gated_apply_tf32x3", st);
                 e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data),
-                                          w->W_type, w->W_ih, w->W_hh, w->b_ih, w->b_hh, m,
+                                          w->W_type, static_cast<const float *>(w->W_ih),
+                                          static_cast<const float *>(w->W_hh), w->b_ih, w->b_hh, m,
                                           reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "gated apply: %s (%s)", cudaGetErrorString(e), why);
+            return SAGA_OK;
+        }
+        case SAGA_SAGE_LSTM: {
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE_LSTM supports BF16 features");
+            if (o.in_dim != 128 || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM supports in_dim 128, out_dim in {64,128,256}");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM act must be NONE/RELU");
+            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "SAGE_LSTM needs W, W_ih, W_hh, b_ih, b_hh");
+            const int F = o.in_dim;
+            __nv_bfloat16 *P = reinterpret_cast<__nv_bfloat16 *>(i0);
+            __nv_bfloat16 *hagg = reinterpret_cast<__nv_bfloat16 *>(i1);
+            const __nv_bfloat16 *Wih = static_cast<const __nv_bfloat16 *>(w->W_ih);
+            for (int gt = 0; gt < 4 && !e; ++gt) {  // P_g = X . W_ih[g] (tensor cores)
+                GemmArgs a;
+                a.M = d.n; a.K0 = F; a.K1 = 0; a.N = F;
+                a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
+                a.W = Wih + (size_t)gt * F * F;
+                a.out = P + (size_t)gt * d.n * F;
+                a.epi = EPI_BIAS_ACT;
+                a.bias = nullptr;
+                a.act = SAGA_ACT_NONE;
+                ProfScope ps_("lstm_input_gemm", st);
+                e = launch_gemm_bf16_tc(a, st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "lstm input gemm: %s (%s)", cudaGetErrorString(e), why);
+            {
+                ProfScope ps_("lstm_gather", st);
+                e = launch_lstm_gather(d, P, static_cast<const __nv_bfloat16 *>(w->W_hh), w->b_ih, w->b_hh, hagg,
+                                       aw.counters, i2, st);
+            }
+            if (e) return cuda_fail(e, "lstm gather");
+            GemmArgs a;
+            a.M = d.n; a.K0 = F; a.K1 = F; a.N = o.out_dim;
+            a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
+            a.A1 = hagg;
+            a.W = static_cast<const __nv_bfloat16 *>(w->W);
+            a.out = static_cast<__nv_bfloat16 *>(out->data);
+            a.epi = EPI_BIAS_ACT;
+            a.bias = w->bias;
+            a.act = o.act;
+            {
+                ProfScope ps_("gemm_bf16_tc", st);
+                e = launch_gemm_bf16_tc(a, st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "sage_lstm gemm: %s (%s)", cudaGetErrorString(e), why);
             return SAGA_OK;
         }
         case SAGA_RGCN: {

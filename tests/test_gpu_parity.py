@@ -96,6 +96,11 @@ def _zoo_inputs(model, n, s, d, seed):
         u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
         return {"H": r(n, 128), "W_type": u(4, 128, 128), "W_ih": u(3, 128, 128), "W_hh": u(3, 128, 128),
                 "b_ih": u(3, 128), "b_hh": u(3, 128)}
+    if model == "sage_lstm":
+        b = 1 / np.sqrt(128)
+        u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
+        return {"X": r(n, 128).bfloat16(), "W_ih": u(4, 128, 128).bfloat16(), "W_hh": u(4, 128, 128).bfloat16(),
+                "b_ih": u(4, 128), "b_hh": u(4, 128), "W": r(256, 128, sc=0.1).bfloat16(), "b": u(128)}
     if model == "rgcn":
         b = 1 / np.sqrt(128)
         u = lambda *sh: (torch.rand(*sh, generator=gen) * 2 - 1) * b
@@ -108,12 +113,13 @@ def _zoo_cfg(model, n, e):
             "sage": W.Config("z", "sage", "er", n, e, False, False, "bf16", (128, 128, 64)),
             "gat": W.Config("z", "gat", "er", n, e, False, False, "bf16", (256, 64), heads=8),
             "gated": W.Config("z", "gated", "er", n, e, False, False, "f32", (128, 128), num_etypes=4),
-            "rgcn": W.Config("z", "rgcn", "er", n, e, False, False, "f32", (128, 128), num_etypes=4)}
+            "rgcn": W.Config("z", "rgcn", "er", n, e, False, False, "f32", (128, 128), num_etypes=4),
+            "sage_lstm": W.Config("z", "sage_lstm", "er", n, e, False, False, "bf16", (128, 128))}
     return base[model]
 
 
 ZOO = [z for z in zoo.zoo(include_big=True) if z[1] > 0]
-MODELS = ["gcn_bf16", "gcn_f32", "sage", "gat", "gated", "rgcn"]
+MODELS = ["gcn_bf16", "gcn_f32", "sage", "gat", "gated", "rgcn", "sage_lstm"]
 
 
 @pytest.mark.parametrize("model", MODELS)
@@ -169,7 +175,7 @@ def test_config_full(saga, cfg):
     _config_check(saga, W.CONFIGS[cfg])
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6", "C7"])
 def test_config_scaled_ragged(saga, cfg):
     """Same recipe at a size that is not a multiple of any tile (ragged tails)."""
     c = W.CONFIGS[cfg]
@@ -179,6 +185,11 @@ def test_config_scaled_ragged(saga, cfg):
 def test_c5_full_sampled(saga):
     """C5 at full size (launch config the bench times), sampled rows incl. hubs."""
     _config_check(saga, W.CONFIGS["C5"], rows_k=3000)
+
+
+def test_c7_full_sampled(saga):
+    """C7 (GraphSAGE-LSTM, NEXT-2) at full size, sampled rows incl. the 16 longest sequences."""
+    _config_check(saga, W.CONFIGS["C7"], rows_k=2000)
 
 
 def test_relabel_invariance_gpu(saga):

@@ -51,7 +51,7 @@ class Config:
     def f_canon(self) -> int:
         """Row width Gather reduces in SAGA order (reading A20)."""
         return {"gcn": self.dims[0], "sage": self.dims[0], "gat": self.dims[-1],
-                "gated": self.dims[0], "rgcn": self.dims[0]}[self.model]
+                "gated": self.dims[0], "rgcn": self.dims[0], "sage_lstm": self.dims[0]}[self.model]
 
     def updates_per_layer(self) -> int:
         """Edge-feature updates of one layer = E * F_canon (reading A20).
@@ -82,6 +82,9 @@ CONFIGS = {
     # SURVEY 8(f) NEXT-3 (not a BASELINE config): R-GCN, C4's graph shape and widths,
     # 4 relation types, fp32, per-type mean + self connection + bias, ReLU
     "C6": Config("C6", "rgcn", "rmat", 1 << 17, 1 << 21, False, False, "f32", (128, 128), num_etypes=4, index=6),
+    # SURVEY 8(f) NEXT-2 (not a BASELINE config): GraphSAGE-LSTM on C2's graph recipe,
+    # bf16 128 -> 128, LSTM hidden 128, ReLU
+    "C7": Config("C7", "sage_lstm", "rmat", 1 << 16, 1 << 20, False, True, "bf16", (128, 128), index=7),
 }
 
 
@@ -328,6 +331,16 @@ def make_inputs(cfg: Config, device="cpu", graph=True):
         d["W_hh"] = uniform(k, "W_hh", 3 * hdim, hdim, bnd, device).view(3, hdim, hdim)
         d["b_ih"] = uniform(k, "b_ih", 3, hdim, bnd, device)
         d["b_hh"] = uniform(k, "b_hh", 3, hdim, bnd, device)
+    elif cfg.model == "sage_lstm":
+        f, fo = cfg.dims
+        bnd = 1.0 / math.sqrt(f)
+        d["X"] = _store(normal(k, f"X/{n}", n, f, 1.0, device), cfg.dtype)
+        d["W_ih"] = _store(uniform(k, "W_ih", 4 * f, f, bnd, device), cfg.dtype).view(4, f, f)
+        d["W_hh"] = _store(uniform(k, "W_hh", 4 * f, f, bnd, device), cfg.dtype).view(4, f, f)
+        d["b_ih"] = uniform(k, "b_ih", 4, f, bnd, device)
+        d["b_hh"] = uniform(k, "b_hh", 4, f, bnd, device)
+        d["W"] = _store(glorot(k, "W", 2 * f, fo, device), cfg.dtype)
+        d["b"] = torch.zeros(fo, dtype=torch.float32, device=device)
     elif cfg.model == "rgcn":
         f, fo = cfg.dims
         T = cfg.num_etypes
