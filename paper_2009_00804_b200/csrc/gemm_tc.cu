@@ -312,12 +312,9 @@ template <int BN>
 cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorMap &mc,
                       int KB, int KB0, const EpiParams &ep, cudaStream_t st) {
     using L = Layout<BN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
-        if (e) return e;
-        attr_set = true;
-    }
+    // per launch: the attribute is per device, and the call is cheap next to the kernel
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e) return e;
     const int64_t ntiles = (a.M + kBM - 1) / kBM;
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);

@@ -369,13 +369,10 @@ cudaError_t launch_tf32split(const CUtensorMap &a0, const CUtensorMap &a1, const
                           const CUtensorMap &blo, int64_t M, int KB, int KB0, int n_tiles, float *msg_out, int ld_out,
                           const GruEpi &gru, cudaStream_t st) {
     using L = Layout<BN>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tf32split<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             L::kBytes);
-        if (e) return e;
-        attr = true;
-    }
+    // per launch: the attribute is per device, and the call is cheap next to the kernel
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tf32split<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kBytes);
+    if (e) return e;
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
