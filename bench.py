@@ -144,7 +144,8 @@ def algorithmic(cfg):
                            "peak": "hbm"}
     elif cfg.model == "gated":
         f, T = cfg.dims[0], cfg.num_etypes
-        out["agg_typed_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f,
+        # typed view (rows (v, t)): col_src, row_ptr of n*T rows, H once, S [n][T][f]
+        out["agg_typed_f32"] = {"bytes": e * 4 + (n * T + 1) * 8 + n * f * 4 + n * T * f * 4, "flops": e * f,
                                 "peak": "hbm"}
         # S read, m written + read, h read twice (GEMM A operand, GRU epilogue), h' written
         out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
@@ -161,8 +162,8 @@ def algorithmic(cfg):
     elif cfg.model == "rgcn":
         f, fo = cfg.dims
         T = cfg.num_etypes
-        out["agg_typed_mean_f32"] = {"bytes": e * 8 + (n + 1) * 8 + n * f * 4 + n * 4 * f * 4, "flops": e * f,
-                                     "peak": "hbm"}
+        out["agg_typed_mean_f32"] = {"bytes": e * 4 + (n * T + 1) * 8 + n * T * 4 + n * f * 4 + n * T * f * 4,
+                                     "flops": e * f, "peak": "hbm"}
         # S read, H read, out written
         out["rgcn_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 + n * fo * 4, "flops": 2 * n * (T + 1) * f * fo,
                                     "peak": "tensor_tf32x3"}

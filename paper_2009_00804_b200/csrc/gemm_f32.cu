@@ -140,8 +140,8 @@ cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, 
                                float *m_ws, float *out, cudaStream_t st) {
     if (M == 0) return cudaSuccess;
     const unsigned gy = (unsigned)((M + BM - 1) / BM);
-    // m = S[M][4f] . W_type viewed as [4f][f]  (types >= T have zero sums)
-    k_sgemm<<<dim3((f + BN - 1) / BN, gy), kThreads, 0, st>>>(M, f, T * f, APlain{S, 4 * f}, BPlain{W_type, f},
+    // m = S[M][T f] . W_type viewed as [T f][f]
+    k_sgemm<<<dim3((f + BN - 1) / BN, gy), kThreads, 0, st>>>(M, f, T * f, APlain{S, T * f}, BPlain{W_type, f},
                                                                EpiStore{m_ws, f});
     cudaError_t e = cudaGetLastError();
     if (e) return e;

@@ -401,7 +401,7 @@ cudaError_t launch_rgcn_apply_tc(int64_t M, int32_t f, int32_t T, const float *S
     cudaError_t e = cudaGetLastError();
     if (e) return e;
     CUtensorMap aS, aH, bh, bl;
-    if (!make_map_f32(&aS, S, M, (int64_t)T * f, 4 * f, kBM) || !make_map_f32(&aH, H, M, f, f, kBM) ||
+    if (!make_map_f32(&aS, S, M, (int64_t)T * f, (int64_t)T * f, kBM) || !make_map_f32(&aH, H, M, f, f, kBM) ||
         !make_map_f32(&bh, b_hi, f, K, K, 128) || !make_map_f32(&bl, b_lo, f, K, K, 128)) {
         *why = "cuTensorMapEncodeTiled failed";
         return cudaErrorInvalidValue;
@@ -427,7 +427,7 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
     cudaError_t e = cudaGetLastError();
     if (e) return e;
     CUtensorMap aS, aM, aH, bmh, bml, bgh, bgl;
-    if (!make_map_f32(&aS, S, M, (int64_t)T * f, 4 * f, kBM) || !make_map_f32(&aM, m_ws, M, f, f, kBM) ||
+    if (!make_map_f32(&aS, S, M, (int64_t)T * f, (int64_t)T * f, kBM) || !make_map_f32(&aM, m_ws, M, f, f, kBM) ||
         !make_map_f32(&aH, H, M, f, f, kBM) || !make_map_f32(&bmh, bm_hi, f, (int64_t)T * f, (int64_t)T * f, 128) ||
         !make_map_f32(&bml, bm_lo, f, (int64_t)T * f, (int64_t)T * f, 128) ||
         !make_map_f32(&bgh, bg_hi, 4 * f, 2 * f, 2 * f, 256) || !make_map_f32(&bgl, bg_lo, 4 * f, 2 * f, 2 * f, 256)) {

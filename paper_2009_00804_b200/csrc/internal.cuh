@@ -32,6 +32,16 @@ struct GraphDev {
     int64_t ntasks = 0;
     int32_t *task_v = nullptr;
     int64_t *task_p = nullptr;
+    // Typed view (built when edge types are given): an internal CSR whose
+    // rows are (destination, type) pairs r = v * num_etypes + t, edges in
+    // (dst, type, COO index) order; the typed gathers (gated, R-GCN) are plain
+    // segment sums over it.  Same merge-path schedule layout as above.
+    int64_t *trow_ptr = nullptr;  // [n * T + 1]
+    int32_t *tcol_src = nullptr;  // [e]
+    float *tinv_deg = nullptr;    // [n * T]  1 / |row| (0 if empty)
+    int64_t ttask_items = 0, tntasks = 0;
+    int32_t *ttask_v = nullptr;
+    int64_t *ttask_p = nullptr;
     cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
 };
 
@@ -62,7 +72,9 @@ cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int3
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
 // GATED typed sums: S[v][t][:] = sum_{type t} H[u]  (fp32)
-// GATED / RGCN typed sums (mean = per-type means, R-GCN): S[v][t][:]  (fp32, fp64 accumulation)
+// GATED / RGCN typed sums over the typed view (mean = per-type means, R-GCN):
+// S[v][t][:] for t < T (layout [n][T][f], fp32 out, fp64 accumulation); without
+// edge types T = 1 and the plain CSR is used.
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,
                                  cudaStream_t st);
 

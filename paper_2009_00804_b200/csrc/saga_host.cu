@@ -119,7 +119,8 @@ struct Plan {
 
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
     Plan p;
-    const size_t nt = (size_t)g.ntasks;
+    // the typed gathers run over the typed view's own schedule
+    const size_t nt = (size_t)std::max(g.ntasks, g.tntasks);
     const size_t n = (size_t)g.n;
     size_t width = 0;
     switch (kind) {
@@ -144,7 +145,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
             p.inter2 = align_up(sizeof(float) * n * 8);                                         // er
             break;
         case SAGA_GATED:
-            p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S
+            p.inter0 = align_up(sizeof(float) * n * (size_t)g.num_etypes * (size_t)std::max(o.in_dim, 0));  // S [n][T][f]
             p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
             p.inter2 = align_up(sizeof(float) * saga::gated_tc_workspace_floats(128, 4));       // split W
             break;
@@ -154,7 +155,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
             p.inter2 = align_up(saga::lstm_workspace_bytes());                                  // staged W_hh^T
             break;
         case SAGA_RGCN:
-            p.inter0 = align_up(sizeof(float) * n * 4 * (size_t)std::max(o.in_dim, 0));        // S (type means)
+            p.inter0 = align_up(sizeof(float) * n * (size_t)g.num_etypes * (size_t)std::max(o.in_dim, 0));  // S (type means)
             p.inter2 = align_up(sizeof(float) * saga::rgcn_tc_workspace_floats(128, 4));        // split W
             break;
     }
@@ -301,7 +302,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i0 = ws + plan.counters + plan.partials;
     uint8_t *i1 = i0 + plan.inter0;
     uint8_t *i2 = i1 + plan.inter1;
-    cudaError_t e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)d.ntasks + 1), st);
+    cudaError_t e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max(d.ntasks, d.tntasks) + 1), st);
     if (e) return cuda_fail(e, "memset counters");
     const char *why = "";
 

@@ -206,3 +206,42 @@ def test_relabel_invariance_gpu(saga):
     yb = H.gpu_step(saga, cfg, H.gpu_graph(saga, cfg, b), b)[0][0]
     err = oracle.rel_err(H.to_np(yb[perm.long().to(DEV)]), H.to_np(ya))
     assert err <= 2e-2
+
+
+@pytest.mark.parametrize("model", ["gated", "rgcn"])
+@pytest.mark.parametrize("T,types", [(1, "none"), (1, "zeros"), (2, "mod"), (3, "skew"), (4, "one_hot_hub")])
+def test_typed_view(saga, model, T, types):
+    """The typed gathers run over the graph's (destination, type) view: every
+    T <= 4, graphs without edge types (T = 1, plain CSR), a type that only a
+    few vertices receive, and a hub whose in-edges are all of one type."""
+    n = 3001
+    rng = np.random.default_rng(5)
+    s = rng.integers(0, n, 40000).astype(np.int32)
+    d = np.minimum(rng.zipf(1.6, 40000) - 1, n - 1).astype(np.int32)  # power-law in-degree
+    d[:5000] = 17                                                        # one hub
+    e = s.shape[0]
+    if types == "none":
+        et = None
+    elif types == "zeros":
+        et = np.zeros(e, np.int32)
+    elif types == "mod":
+        et = (np.arange(e) % 2).astype(np.int32)
+    elif types == "skew":
+        et = np.where(np.arange(e) % 97 == 0, 2, np.arange(e) % 2).astype(np.int32)
+    else:
+        et = (np.arange(e) % 4).astype(np.int32)
+        et[d == 17] = 3
+    cfg = W.Config("tv", model, "er", n, e, False, False, "f32", (128, 128), num_etypes=T)
+    x = _zoo_inputs(model, n, s, d, 11)
+    x["W_type"] = x["W_type"][:T].contiguous()
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    if et is not None:
+        x["etype"] = torch.from_numpy(et)
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, _ = H.gpu_step(saga, cfg, g, dx)
+    torch.cuda.synchronize()
+    og = H.oracle_graph(oracle, cfg, x)
+    refs = H.oracle_step(oracle, cfg, og, x)
+    err = oracle.rel_err(H.to_np(outs[0]), refs[0])
+    assert err <= H.TOL["f32"], f"{model} T={T} {types}: rel err {err:.3e}"
