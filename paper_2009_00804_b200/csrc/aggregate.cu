@@ -102,10 +102,9 @@ struct SumBf16Op {
 #pragma unroll
         for (int i = 0; i < NB; ++i) c.a[i] = 0.0f;
     }
-    // row u, lane slice: one IMAD.WIDE.U32 per address (row byte offsets stay
-    // below 2^32 for every N saga_layer accepts)
+    // row u, lane slice: one IMAD.WIDE.U32 per address
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        const char *p = reinterpret_cast<const char *>(X) + lane * (2 * NB) + (uint64_t)(uint32_t)u * (64u * NB);
+        const char *p = ptx::mad_wide((uint32_t)u, 64u * NB, reinterpret_cast<const char *>(X) + lane * (2 * NB));
         Val v;
         if constexpr (NB == 8) {
             const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p));
@@ -175,7 +174,8 @@ struct GcnF32FusedOp {
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
         Val v;
         v.w = __ldg(dinv + u);
-        const float *p = X + (int64_t)u * f_in + lane * NPL;
+        const float *p = reinterpret_cast<const float *>(
+            ptx::mad_wide((uint32_t)u, 4u * (uint32_t)f_in, reinterpret_cast<const char *>(X + lane * NPL)));
         const bool on = lane * NPL < f_in;
         if constexpr (NPL == 4) {
             const float4 x = on ? __ldg(reinterpret_cast<const float4 *>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -240,9 +240,10 @@ struct GatOp {
     __device__ __forceinline__ void zero(Acc &c) const { c.m = -INFINITY; c.l = 0.f; c.a0 = 0.f; c.a1 = 0.f; }
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
         Val v;
-        const uint64_t uu = (uint32_t)u;
-        v.z2 = __ldg(reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(z) + lane * 4 + uu * 128u));
-        v.el = __ldg(reinterpret_cast<const float *>(reinterpret_cast<const char *>(el) + (lane >> 2) * 4 + uu * 32u));
+        v.z2 = __ldg(reinterpret_cast<const uint32_t *>(
+            ptx::mad_wide((uint32_t)u, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
+        v.el = __ldg(reinterpret_cast<const float *>(
+            ptx::mad_wide((uint32_t)u, 32u, reinterpret_cast<const char *>(el) + (lane >> 2) * 4)));
         return v;
     }
     // A whole batch of one row (the engine's fast path): one rescale of the
@@ -334,7 +335,7 @@ struct SumF32Op {
         for (int i = 0; i < 4; ++i) c.a[i] = 0.0;
     }
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        const char *p = reinterpret_cast<const char *>(H) + lane * 16 + (uint64_t)(uint32_t)u * 512u;
+        const char *p = ptx::mad_wide((uint32_t)u, 512u, reinterpret_cast<const char *>(H) + lane * 16);
         return Val{__ldg(reinterpret_cast<const float4 *>(p))};
     }
     static constexpr bool kBatchAdd = true;

@@ -259,5 +259,14 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
     return f;
 }
 
+// base + (uint64)a * b as ONE IMAD.WIDE.U32 with a 64-bit addend: written in
+// C++ the compiler re-associates a row gather's address into
+// (a * stride | lane offset) + base, four instructions per load.
+__device__ __forceinline__ const char *mad_wide(uint32_t a, uint32_t b, const void *base) {
+    const char *r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(base));
+    return r;
+}
+
 }  // namespace ptx
 }  // namespace saga
