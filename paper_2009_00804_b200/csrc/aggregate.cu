@@ -507,15 +507,18 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         const int32_t q = base + lane;
         return q < p1 ? __ldcs(g.col_src + q) : 0;
     };
+    // col_src in 32-edge chunks, two chunks ahead of the one in use (one
+    // chunk -- 4 batches -- left 10% of the C5 stalls on the col_src load)
     int32_t cb = p;
-    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32);
+    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32), cs_c = load_cs(cb + 64);
     // keeps q - cb < 32; batches start at p + multiple of U and U | 32, so a
     // batch never straddles a chunk
     auto slide = [&](int32_t q) {
         if (q - cb >= 32) {
             cb += 32;
             cs_a = cs_b;
-            cs_b = load_cs(cb + 32);
+            cs_b = cs_c;
+            cs_c = load_cs(cb + 64);
         }
     };
 
