@@ -21,10 +21,10 @@ LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)
     "C1": [("GcnF32FusedOp", "gcn_f32_fused")],
     "C2": [("SumBf16Op", "agg_mean_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C3": [("GatDenseOp", "gat_edge"), ("GatOp", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
-    "C4": [("TypedF32Op", "agg_typed_f32"), ("k_sgemm", "gated_apply_sgemm"), ("k_gemm_tf32split", "gated_apply_tf32x3")],
+    "C4": [("SumF32Op", "agg_typed_f32"), ("TypedF32Op", "agg_typed_f32"), ("k_sgemm", "gated_apply_sgemm"), ("k_gemm_tf32split", "gated_apply_tf32x3")],
     "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
-    "C6": [("TypedF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3")],
-    "C7": [("k_lstm_gather", "lstm_gather")],
+    "C6": [("SumF32Op", "agg_typed_mean_f32"), ("TypedF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3")],
+    "C7": [("k_lstm_gather", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
 }
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram_read"),
         ("dram__bytes_write.sum", "dram_write"), ("lts__t_sector_hit_rate.pct", "L2_hit_%"),
