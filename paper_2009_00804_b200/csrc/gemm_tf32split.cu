@@ -7,8 +7,9 @@
 // (sum_e H[u] W_t(e) = sum_t S_t W_t).  Two GEMMs:
 //   messages:  m[M][128]   = [S_0 || .. || S_{T-1}] . [W_0; ..; W_{T-1}]   (K = 128 T)
 //   gates:     G[M][4x128] = [m || h] . B_gru  with, per hidden unit j, the
-//              columns r_j, z_j (K = 256), gin_j (m rows only), ghn_j (h rows
-//              only), followed by the PyTorch-GRUCell epilogue (reading A15):
+//              columns gin_j (m rows only), r_j, z_j (K = 256), ghn_j (h rows
+//              only) -- the MMAs skip the two zero blocks (N = 192 per K half)
+//              -- followed by the PyTorch-GRUCell epilogue (reading A15):
 //              h' = (1 - z) tanh(gin + b_in + r (ghn + b_hn)) + z h.
 // The fp32 tolerance (1e-4) rules out single-pass TF32 (~3e-4 normwise), so
 // every operand is split x = x_hi + x_lo with x_hi = tf32(x) and x_lo =
@@ -147,6 +148,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ============================ MMA issuer ==============================
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::make_idesc(2 /*TF32*/, kBM, BN);
+            // GRU tiles hold columns [gin | r | z | ghn] x 64 units: the m rows
+            // of K (kb < KB0) never reach ghn and the h rows never reach gin,
+            // so after the first K step (N = 256, which zeroes every column)
+            // the m part runs N = 192 over [gin r z] and the h part N = 192
+            // over [r z ghn] -- 25% fewer MMAs
+            constexpr uint32_t idesc192 = ptx::make_idesc(2 /*TF32*/, kBM, 192);
+            constexpr uint32_t kRow64 = 64 * 128;  // 64 B^T rows (1024-B aligned swizzle atoms)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -164,6 +172,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int k = 0; k < kBK / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
                         const uint32_t off = k * 32;
+                        if (EPI == EPI_GRU && (kb | k) != 0) {
+                            const bool hpart = kb >= KB0;
+                            const uint32_t dd = d + (hpart ? 64 : 0), bo = hpart ? kRow64 : 0;
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(bhi + bo + off),
+                                           idesc192, 1);
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + bo + off),
+                                           idesc192, 1);
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(bhi + bo + off),
+                                           idesc192, 1);
+                            continue;
+                        }
                         ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(bhi + off), idesc,
                                        (kb | k) != 0);
                         ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + off), idesc, 1);
@@ -232,12 +251,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                // tile columns: [r | z | gin | ghn] x 64 units (unit0 = 64 nt)
+                // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt)
 #pragma unroll 1
                 for (int c = 0; c < 2; ++c) {
                     uint32_t vr[32], vz[32];
-                    ptx::tmem_ld32(tbase + c * 32, vr);
-                    ptx::tmem_ld32(tbase + 64 + c * 32, vz);
+                    ptx::tmem_ld32(tbase + 64 + c * 32, vr);
+                    ptx::tmem_ld32(tbase + 128 + c * 32, vz);
                     ptx::tmem_ld_wait();
                     const int j0 = nt * 64 + c * 32;
                     float rg[32], zg[32];
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                           __ldg(gru.b_hh + 128 + j0 + j));
                     }
                     uint32_t vi[32], vh[32];
-                    ptx::tmem_ld32(tbase + 128 + c * 32, vi);
+                    ptx::tmem_ld32(tbase + c * 32, vi);
                     ptx::tmem_ld32(tbase + 192 + c * 32, vh);
                     ptx::tmem_ld_wait();
                     if (row < M) {
@@ -285,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // B^T operands in K-major layout, split hi/lo:
 //   messages: Bm[n][k] = W_type[k / f][k % f][n]             (N = f, K = T f)
-//   gates:    Bg[c][k], c = 256 nt + 64 g + j (unit 64 nt + j; g = r, z, gin, ghn),
+//   gates:    Bg[c][k], c = 256 nt + 64 s + j (unit 64 nt + j; slot s = gin, r, z, ghn),
 //             k < f from W_ih, k >= f from W_hh; gin has no h rows, ghn no m rows.
 __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_ih,
                                 const float *__restrict__ W_hh, float *bm_hi, float *bm_lo, float *bg_hi,
@@ -302,14 +321,14 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
         } else {
             idx = i - nm;
             const int c = idx / (2 * f), k = idx % (2 * f);
-            const int nt = c / 256, g = (c % 256) / 64, j = nt * 64 + c % 64;
+            const int nt = c / 256, slot = (c % 256) / 64, j = nt * 64 + c % 64;
             const bool from_m = k < f;
             const int kk = from_m ? k : k - f;
-            if (g < 2)
-                x = (from_m ? W_ih : W_hh)[((int64_t)g * f + kk) * f + j];
-            else if (g == 2)
+            if (slot == 1 || slot == 2)  // r (gate 0), z (gate 1)
+                x = (from_m ? W_ih : W_hh)[((int64_t)(slot - 1) * f + kk) * f + j];
+            else if (slot == 0)          // gin: m rows only
                 x = from_m ? W_ih[((int64_t)2 * f + kk) * f + j] : 0.0f;
-            else
+            else                         // ghn: h rows only
                 x = from_m ? 0.0f : W_hh[((int64_t)2 * f + kk) * f + j];
             hi = bg_hi; lo = bg_lo;
         }
