@@ -14,14 +14,17 @@
 //     takes the next vertex from a queue in descending in-degree order (the
 //     graph's deg_order): the longest sequences -- the critical path --
 //     start first on whole SMs and the short ones fill in behind them;
-//   * thread (gate g, unit j) computes z_g[j] = P_g[u][j] + b + h . W_hh[g][:, j]
+//   * thread (unit j, gate g) computes z_g[j] = P_g[u][j] + b + h . W_hh[g][:, j]
 //     with its row of W_hh^T (128 bf16) resident in 64 registers -- a step
 //     reads only h (bf16, 256 B, broadcast) from shared memory; re-reading a
 //     128 KB shared-memory W_hh every step was the bound (ncu: MIO throttle,
 //     1.6K shared wavefronts per step).  Each product is one sm_100
-//     mixed-precision FHFMA.BF16 (bf16 x bf16 -> fp32 accumulate), the
-//     thread applies its gate's activation, and the gate-0 thread of unit j
-//     keeps c_j (fp32) in a register and writes h_j;
+//     mixed-precision FHFMA.BF16 (bf16 x bf16 -> fp32 accumulate);
+//   * the 4 gates of unit j sit in adjacent lanes: after its activation each
+//     thread gathers (i, f, g, o) with shuffles and updates c_j (fp32, kept
+//     identically in the 4 lanes), and h is double-buffered, so a step has
+//     one barrier (the h broadcast) instead of a gate exchange and a
+//     broadcast through shared memory;
 //   * the P terms of the next kAhead steps are in flight while a step runs.
 // Reading A25: sequence = in-edges in CSR order, PyTorch
 // LSTMCell (i, f, g, o), zero initial state, output = final h (0 without
@@ -38,22 +41,23 @@ namespace saga {
 namespace {
 
 constexpr int kF = 128;        // hidden = input width
-constexpr int kThreads = 512;  // one thread per (gate, unit): 4 x 128
+constexpr int kThreads = 512;  // one thread per (unit, gate): 128 x 4
 constexpr int kAhead = 2;      // steps of P prefetched ahead
 
 struct LstmSmem {
-    uint4 hb[kF / 8];          // current hidden state, bf16 (the recurrent GEMV operand)
-    float z[4][kF];            // gate activations i, f, g, o
+    uint4 hb[2][kF / 8];       // hidden state, bf16, double-buffered (read t & 1, write (t + 1) & 1)
     int32_t v;                 // current vertex
 };
 
-__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// sigm(x) = 1 / (1 + e^-x) with the fast reciprocal (|error| ~1e-7, the
+// output feeds bf16 h); tanh(x) = 2 sigm(2x) - 1
+__device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
-// wt[g][j][c] = W_hh[g][8c .. 8c+7][j] (bf16): row (g, j) of W_hh^T, 256 contiguous bytes
+// wt[j][g][c] = W_hh[g][8c .. 8c+7][j] (bf16): row (unit j, gate g) of W_hh^T, 256 contiguous bytes
 __global__ void k_stage_whh(const __nv_bfloat16 *__restrict__ W_hh, uint4 *wt) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over 4 * kF * kF / 8 chunks
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over kF * 4 * kF / 8 chunks
     if (i >= 4 * kF * kF / 8) return;
-    const int c = i % (kF / 8), j = (i / (kF / 8)) % kF, g = i / (kF / 8 * kF);
+    const int c = i % (kF / 8), g = (i / (kF / 8)) % 4, j = i / (kF / 8 * 4);
     uint32_t q[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -71,13 +75,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const float *__restrict__ b_ih, const float *__restrict__ b_hh,          // [4][kF]
                   __nv_bfloat16 *__restrict__ h_out, int32_t *queue) {
     __shared__ LstmSmem S;
-    // thread -> (gate g, unit j); a warp is 32 consecutive units of one gate,
-    // so every h read is a broadcast
-    const int g = threadIdx.x / kF, j = threadIdx.x % kF;
+    // thread -> (unit j, gate g): the 4 gates of a unit are adjacent lanes,
+    // so the cell update gathers them with shuffles and a step needs ONE
+    // barrier (the h broadcast)
+    const int j = threadIdx.x / 4, g = threadIdx.x % 4;
+    const int lane = threadIdx.x & 31, gbase = lane & ~3;
     uint4 w[kF / 8];  // this thread's row of W_hh^T, resident in registers
 #pragma unroll
-    for (int c = 0; c < kF / 8; ++c) w[c] = __ldg(wt + ((int64_t)g * kF + j) * (kF / 8) + c);
+    for (int c = 0; c < kF / 8; ++c) w[c] = __ldg(wt + ((int64_t)j * 4 + g) * (kF / 8) + c);
     const float bias = __ldg(b_ih + g * kF + j) + __ldg(b_hh + g * kF + j);
+    const float ks = g == 2 ? 2.0f : 1.0f;  // gate g uses tanh = 2 sigm(2x) - 1
     const __nv_bfloat16 *Pg = P + g * (int64_t)n * kF + j;
 
     for (;;) {
@@ -85,17 +92,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int32_t qi = atomicAdd(queue, 1);
             S.v = qi < n ? order[qi] : -1;
         }
-        if (threadIdx.x < kF / 8) S.hb[threadIdx.x] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x < kF / 8) S.hb[0][threadIdx.x] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         const int32_t v = S.v;
         if (v < 0) break;
-        const int64_t p0 = row_ptr[v], p1 = row_ptr[v + 1];
-        float c = 0.0f, hf = 0.0f;  // cell state and output of unit j (gate-0 threads)
+        const int32_t p0 = (int32_t)row_ptr[v], p1 = (int32_t)row_ptr[v + 1];
+        float c = 0.0f, hf = 0.0f;  // cell state and output of unit j (identical in its 4 lanes)
         __nv_bfloat16 ring[kAhead];
 #pragma unroll
         for (int a = 0; a < kAhead; ++a)
             ring[a] = (p0 + a < p1) ? Pg[(int64_t)__ldg(col_src + p0 + a) * kF] : __float2bfloat16_rn(0.0f);
-        for (int64_t p = p0; p < p1; ++p) {
+        int buf = 0;
+        for (int32_t p = p0; p < p1; ++p) {
             const float pz = __bfloat162float(ring[0]);
 #pragma unroll
             for (int a = 0; a + 1 < kAhead; ++a) ring[a] = ring[a + 1];
@@ -103,26 +111,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 (p + kAhead < p1) ? Pg[(int64_t)__ldg(col_src + p + kAhead) * kF] : __float2bfloat16_rn(0.0f);
             // z_g[j] = P_g[u][j] + b + h . W_hh[g][:, j]: 64 FHFMA.BF16 in 4 chains
             float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const uint4 *hb = S.hb[buf];
 #pragma unroll
             for (int cc = 0; cc < kF / 8; ++cc) {
-                const uint4 hv = S.hb[cc];
+                const uint4 hv = hb[cc];
                 ptx::fma_bf16x2_f32(a4[0], w[cc].x, hv.x);
                 ptx::fma_bf16x2_f32(a4[1], w[cc].y, hv.y);
                 ptx::fma_bf16x2_f32(a4[2], w[cc].z, hv.z);
                 ptx::fma_bf16x2_f32(a4[3], w[cc].w, hv.w);
             }
             const float zz = (a4[0] + a4[1]) + (a4[2] + a4[3]) + pz + bias;
-            S.z[g][j] = g == 2 ? tanhf(zz) : sigm(zz);
-            __syncthreads();  // all gates written, all reads of h done
-            if (g == 0) {
-                c = S.z[1][j] * c + S.z[0][j] * S.z[2][j];
-                hf = S.z[3][j] * tanhf(c);
-                reinterpret_cast<__nv_bfloat16 *>(S.hb)[j] = __float2bfloat16_rn(hf);
-            }
-            __syncthreads();  // new h visible
+            const float sg = sigm_fast(ks * zz);
+            const float act = g == 2 ? 2.0f * sg - 1.0f : sg;
+            const float ig = __shfl_sync(0xffffffffu, act, gbase + 0);
+            const float fg = __shfl_sync(0xffffffffu, act, gbase + 1);
+            const float gg = __shfl_sync(0xffffffffu, act, gbase + 2);
+            const float og = __shfl_sync(0xffffffffu, act, gbase + 3);
+            c = fg * c + ig * gg;
+            hf = og * (2.0f * sigm_fast(2.0f * c) - 1.0f);
+            buf ^= 1;
+            if (g == 0) reinterpret_cast<__nv_bfloat16 *>(S.hb[buf])[j] = __float2bfloat16_rn(hf);
+            __syncthreads();  // new h visible; every read of the old one is done
         }
         if (g == 0) h_out[(int64_t)v * kF + j] = __float2bfloat16_rn(hf);
-        __syncthreads();  // h read before the next sequence resets it
+        __syncthreads();  // S.v and S.hb[0] are rewritten for the next sequence
     }
 }
 
