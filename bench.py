@@ -437,15 +437,27 @@ def run_e2e(args, cfg, saga, H, d, dev, ws):
     weights_dev = {k: v for k, v in d.items() if k not in ("src", "dst", "etype", "X", "H")}
     out_host = None
     times = []
+    copy_stream = torch.cuda.Stream(dev)
     for it in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        main = torch.cuda.current_stream(dev)
         dd = dict(weights_dev)
-        for k in ("src", "dst", "etype") + tuple(feats):
+        for k in ("src", "dst", "etype"):
             if k in host and host[k] is not None:
                 dd[k] = host[k].to(dev, non_blocking=True)
         dd.setdefault("etype", None)
+        # the feature rows travel on a copy stream while the graph is built
+        # from the COO (the build does not read them)
+        with torch.cuda.stream(copy_stream):
+            for k in feats:
+                dd[k] = host[k].to(dev, non_blocking=True)
+            fe = torch.cuda.Event()
+            fe.record(copy_stream)
         g = H.gpu_graph(saga, cfg, dd)
+        main.wait_event(fe)
+        for k in feats:
+            dd[k].record_stream(main)
         outs, _ = H.gpu_step(saga, cfg, g, dd)
         if out_host is None:
             out_host = torch.empty(outs[-1].shape, dtype=outs[-1].dtype, pin_memory=True)
@@ -460,7 +472,8 @@ def run_e2e(args, cfg, saga, H, d, dev, ws):
     return {"value": job_value(cfg.layer_updates(), len(times), ws, tmax * 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * tmax / len(times),
-            "includes": "H2D COO+features, saga_graph_build, layer, D2H output"}
+            "includes": "H2D COO+features (features on a copy stream, overlapping the graph build), "
+                        "saga_graph_build, layer, D2H output"}
 
 
 def main():
