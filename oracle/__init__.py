@@ -53,6 +53,9 @@ def lib():
         L.oracle_gated.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, P, P, P, P, i64, P]
         L.oracle_sage_lstm.restype = None
         L.oracle_sage_lstm.argtypes = [i32, P, P, P, ctypes.c_int, i32, P, P, P, P, P, i32, P, ctypes.c_int, P, i64, P]
+        L.oracle_ggnn.restype = None
+        L.oracle_ggnn.argtypes = [i32, P, P, P, ctypes.c_int, i32, P, P, ctypes.c_int, ctypes.c_int,
+                                  P, P, P, P, P, i64, P]
         L.oracle_rgcn.restype = None
         L.oracle_rgcn.argtypes = [i32, P, P, P, i32, P, ctypes.c_int, i32, P, P, i32, P, ctypes.c_int, P, i64, P]
         _lib = L
@@ -226,6 +229,22 @@ def sage_lstm(g: CSR, X, W_ih, W_hh, b_ih, b_hh, W, b=None, act=1, rows=None):
     out = np.zeros((nr, f_out), np.float64)
     lib().oracle_sage_lstm(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(x), xd, f, _ptr(Wi), _ptr(Wh),
                            _ptr(_f64(b_ih)), _ptr(_f64(b_hh)), _ptr(Wm), f_out, _ptr(bb), act, _ptr(r), nr, _ptr(out))
+    return out
+
+
+def ggnn(g: CSR, H, W_e, b_e, W_ih, W_hh, b_ih, b_hh, act=1, agg="sum", rows=None):
+    """Paper-form GGNN layer (oracle.c oracle_ggnn; reading A26): per-edge
+    MLP on [H[u] || H[v]], sum (or max) over in-edges, GRUCell."""
+    x, xd = _features(H)
+    We = _f64(W_e)
+    f = We.shape[1]
+    assert We.shape == (2 * f, f)
+    be = None if b_e is None else _f64(b_e)
+    r, nr = _rows(rows, g.n)
+    out = np.zeros((nr, f), np.float64)
+    lib().oracle_ggnn(g.n, _ptr(g.row_ptr), _ptr(g.col_src), _ptr(x), xd, f, _ptr(We), _ptr(be), act,
+                      1 if agg == "max" else 0, _ptr(_f64(W_ih)), _ptr(_f64(W_hh)), _ptr(_f64(b_ih)),
+                      _ptr(_f64(b_hh)), _ptr(r), nr, _ptr(out))
     return out
 
 

@@ -415,3 +415,70 @@ void oracle_sage_lstm(int32_t n, const int64_t *row_ptr, const int32_t *col_src,
         free(h); free(c); free(z); free(hn);
     }
 }
+
+/* ------------------------------------------------------------------------
+ * Paper-form GGNN layer.
+ * (the GGNN walkthrough) and Table 1, taken literally (reading A26):
+ *   Scatter:     x_e = [H[u] || H[v]]                 (e = u -> v, 2f wide)
+ *   ApplyEdge:   y_e = act(x_e . W_e + b_e)           (a one-layer MLP, W_e [2f][f])
+ *   Gather:      m[v] = sum_{e into v} y_e            ("sums the edge^{l+1} of all
+ *                its inedges"; agg = 1 takes the elementwise max instead,
+ *                the max of line 218); 0 for a vertex without in-edges
+ *   ApplyVertex: h' = GRUCell(m[v], H[v])             (gate order r, z, n, reading A15)
+ * act 0 none / 1 ReLU.  W_ih [3][f][f], W_hh [3][f][f], b_* [3][f].
+ * ---------------------------------------------------------------------- */
+void oracle_ggnn(int32_t n, const int64_t *row_ptr, const int32_t *col_src, const void *x, int x_dtype,
+                 int32_t f, const double *W_e, const double *b_e, int act, int agg,
+                 const double *W_ih, const double *W_hh, const double *b_ih, const double *b_hh,
+                 const int64_t *rows, int64_t nrows, double *out) {
+    if (!rows) nrows = n;
+#pragma omp parallel
+    {
+        double *xe = (double *)malloc(sizeof(double) * 2 * (size_t)f);
+        double *y = (double *)malloc(sizeof(double) * (size_t)f);
+        double *m = (double *)malloc(sizeof(double) * (size_t)f);
+        double *h = (double *)malloc(sizeof(double) * (size_t)f);
+        double *gi = (double *)malloc(sizeof(double) * 3 * (size_t)f);
+        double *gh = (double *)malloc(sizeof(double) * 3 * (size_t)f);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < nrows; ++i) {
+            int64_t v = row_at(rows, i);
+            int64_t p0 = row_ptr[v], p1 = row_ptr[v + 1];
+            for (int32_t j = 0; j < f; ++j) m[j] = 0.0;
+            for (int64_t p = p0; p < p1; ++p) {
+                int32_t u = col_src[p];
+                for (int32_t k = 0; k < f; ++k) {                                   /* Scatter */
+                    xe[k] = load_x(x, x_dtype, u, f, k);
+                    xe[f + k] = load_x(x, x_dtype, v, f, k);
+                }
+                for (int32_t j = 0; j < f; ++j) y[j] = b_e ? b_e[j] : 0.0;          /* ApplyEdge */
+                for (int32_t k = 0; k < 2 * f; ++k)
+                    for (int32_t j = 0; j < f; ++j) y[j] += xe[k] * W_e[(int64_t)k * f + j];
+                if (act == 1)
+                    for (int32_t j = 0; j < f; ++j) y[j] = y[j] > 0.0 ? y[j] : 0.0;
+                for (int32_t j = 0; j < f; ++j)                                     /* Gather */
+                    m[j] = (agg == 1 && p > p0) ? (y[j] > m[j] ? y[j] : m[j]) : (agg == 1 ? y[j] : m[j] + y[j]);
+            }
+            for (int32_t k = 0; k < f; ++k) h[k] = load_x(x, x_dtype, v, f, k);    /* ApplyVertex */
+            for (int32_t g = 0; g < 3; ++g)
+                for (int32_t j = 0; j < f; ++j) {
+                    gi[g * f + j] = b_ih[g * f + j];
+                    gh[g * f + j] = b_hh[g * f + j];
+                }
+            for (int32_t g = 0; g < 3; ++g)
+                for (int32_t k = 0; k < f; ++k)
+                    for (int32_t j = 0; j < f; ++j) {
+                        gi[g * f + j] += m[k] * W_ih[((int64_t)g * f + k) * f + j];
+                        gh[g * f + j] += h[k] * W_hh[((int64_t)g * f + k) * f + j];
+                    }
+            double *o = out + i * (int64_t)f;
+            for (int32_t j = 0; j < f; ++j) {
+                double r = sigmoid(gi[j] + gh[j]);
+                double zg = sigmoid(gi[f + j] + gh[f + j]);
+                double ng = tanh(gi[2 * f + j] + r * gh[2 * f + j]);
+                o[j] = (1.0 - zg) * ng + zg * h[j];
+            }
+        }
+        free(xe); free(y); free(m); free(h); free(gi); free(gh);
+    }
+}
