@@ -167,6 +167,16 @@ def algorithmic(cfg):
         # S read, H read, out written
         out["rgcn_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 + n * fo * 4, "flops": 2 * n * (T + 1) * f * fo,
                                     "peak": "tensor_tf32x3"}
+    elif cfg.model == "ggnn":
+        f = cfg.dims[0]
+        # AB = H . [W_a | W_b] + [0 | b_e]: H read, AB written (K = f, N = 2f)
+        out["ggnn_edge_tf32x3"] = {"bytes": n * f * 4 + n * 2 * f * 4, "flops": 2 * n * f * 2 * f,
+                                   "peak": "tensor_tf32x3"}
+        # per edge an A row (512 B); per row its B half and the m row written
+        out["agg_edge_mlp_f32"] = {"bytes": e * 4 + (n + 1) * 8 + e * f * 4 + n * f * 4 + n * f * 4,
+                                   "flops": 3 * e * f, "peak": "hbm"}
+        # GRU over [m || h]: m, h read (h twice), h' written
+        out["ggnn_gru_tf32x3"] = {"bytes": n * f * 4 * 4, "flops": 2 * n * 6 * f * f, "peak": "tensor_tf32x3"}
     return out
 
 
@@ -315,7 +325,8 @@ def workload_config(cfg):
             "C4": "gated GRU fp32, R-MAT N=2^17 E=2^21, 4 edge types, 128",
             "C5": "GCN at scale bf16, R-MAT N=2^22 E=2^26+self-loops, 256->256",
             "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128",
-            "C7": "GraphSAGE-LSTM bf16 (NEXT-2), R-MAT N=2^16 E=2^20 distinct, 128->128"}
+            "C7": "GraphSAGE-LSTM bf16 (NEXT-2), R-MAT N=2^16 E=2^20 distinct, 128->128",
+            "C8": "paper-form GGNN fp32 (NEXT-4: edge MLP on [h_src||h_dst] + ReLU, sum, GRU), R-MAT N=2^17 E=2^21, 128"}
     return {"workload": f"{cfg.name}: {desc.get(cfg.name, cfg.name)}", "vertices": cfg.n, "edges": cfg.num_edges,
             "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
 

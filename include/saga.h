@@ -7,7 +7,7 @@
  * (Section 2; Table 1 `tbl:benchmark`, lines
  * 176-180).  The operations and their exact definitions are the ones the
  * fp64 oracle (oracle/oracle.c) writes out; DESIGN.md lists every reading of
- * the paper they rest on (A1..A23).
+ * the paper they rest on (A1..A26).
  *
  * Conventions shared by every entry point
  *  - All array arguments are DEVICE pointers (CUDA global memory on the
@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SAGA_ABI_VERSION 1
+#define SAGA_ABI_VERSION 2  /* 2: SAGA_GGNN, saga_layer_opts.aggregator */
 
 #if defined(__GNUC__)
 #define SAGA_API __attribute__((visibility("default")))
@@ -63,8 +63,12 @@ typedef enum {
     SAGA_GAT = 2,   /* ApplyEdge attention score, Gather attention(in_edges), ELU              */
     SAGA_GATED = 3, /* per-edge-type message W_t, Gather sum(in_edges), ApplyVertex GRU        */
     SAGA_RGCN = 4,  /* per-type mean messages W_t + self term, ApplyVertex sum */
-    SAGA_SAGE_LSTM = 5 /* Gather LSTM(in_edges) + vertex, ApplyVertex MLP     */
+    SAGA_SAGE_LSTM = 5, /* Gather LSTM(in_edges) + vertex, ApplyVertex MLP    */
+    SAGA_GGNN = 6   /* Scatter src&dst, ApplyEdge MLP, Gather sum|max, ApplyVertex GRU (NEXT-4) */
 } saga_model;
+
+/* Gather reduction of SAGA_GGNN (line 218: "sum/mean/max"). */
+typedef enum { SAGA_AGG_SUM = 0, SAGA_AGG_MAX = 1 } saga_aggregator;
 
 typedef enum { SAGA_ACT_NONE = 0, SAGA_ACT_RELU = 1, SAGA_ACT_ELU = 2 } saga_act;
 
@@ -84,22 +88,24 @@ typedef struct {
     int32_t act;              /* saga_act applied by ApplyVertex: GCN/SAGE (RELU or NONE); */
                               /* GAT must be ELU; GATED ignores it (GRU)                   */
     float leaky_slope;        /* GAT LeakyReLU negative slope in [0, 1] (0.2 in config C3) */
+    int32_t aggregator;       /* saga_aggregator, GGNN only (else ignored)                 */
 } saga_layer_opts;
 
 /* Weights (device, row-major, [in][out] orientation = x . W, reading A8).
  * Unused members may be NULL.                                               */
 typedef struct {
     const void *W;         /* GCN [in][out]; SAGE [2*in][out] (self rows first); GAT [in][heads*hd];
-                              RGCN: W_self [in][out] fp32; dtype = features dtype                 */
-    const float *bias;     /* [out] fp32, nullable (= 0)                                           */
+                              RGCN: W_self [in][out] fp32; GGNN: edge MLP W_e [2*in][in] fp32
+                              (source rows first); dtype = features dtype                         */
+    const float *bias;     /* [out] fp32, nullable (= 0); GGNN: the edge MLP bias b_e [in]          */
     const float *attn_src; /* GAT [heads][hd] fp32 (applied to the source z)                      */
     const float *attn_dst; /* GAT [heads][hd] fp32 (applied to the destination z)                 */
     const float *W_type;   /* GATED, RGCN [T][f][f] fp32                                           */
-    const void *W_ih;      /* GATED [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form);
+    const void *W_ih;      /* GATED, GGNN [3][f][f] fp32, gate order r, z, n (PyTorch GRUCell form);
                               SAGE_LSTM [4][f][f] bf16, gate order i, f, g, o (LSTMCell form)    */
-    const void *W_hh;      /* GATED [3][f][f] fp32; SAGE_LSTM [4][f][f] bf16                     */
-    const float *b_ih;     /* GATED [3][f], SAGE_LSTM [4][f] fp32                                  */
-    const float *b_hh;     /* GATED [3][f], SAGE_LSTM [4][f] fp32                                  */
+    const void *W_hh;      /* GATED, GGNN [3][f][f] fp32; SAGE_LSTM [4][f][f] bf16               */
+    const float *b_ih;     /* GATED, GGNN [3][f], SAGE_LSTM [4][f] fp32                            */
+    const float *b_hh;     /* GATED, GGNN [3][f], SAGE_LSTM [4][f] fp32                            */
 } saga_weights;
 
 /* Returns SAGA_ABI_VERSION. */
@@ -180,6 +186,11 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *        out[v] = act( sum_t mean_{u->v, type t} x[u] . W_type[t] + x[v] . W + bias )
  *        (a type with no in-edges of v contributes 0); F32, in_dim = out_dim
  *        = 128, num_etypes <= 4, act NONE or RELU.
+ *  GGNN  (lines 142-147, Table 1; A26):
+ *        y(u->v) = act([x[u] || x[v]] . W_e + b_e)   (act = opts.act, NONE or RELU)
+ *        m[v] = sum (or elementwise max, opts.aggregator) of y over v's in-edges,
+ *        0 without in-edges; out[v] = GRUCell(m[v], x[v]) (weights as GATED)
+ *        F32, in_dim = out_dim = 128; edge types are ignored.
  *  features  [N][in_dim];  out  [N][out_dim] with the features' dtype
  *  workspace device scratch of at least saga_layer_workspace_bytes() bytes;
  *            contents on entry are ignored; it must not be shared by calls in

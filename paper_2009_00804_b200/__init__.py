@@ -23,10 +23,11 @@ LIB_PATH = os.path.join(_HERE, "libsaga.so")
 SAGA_OK, SAGA_EINVAL, SAGA_ERANGE, SAGA_ESHAPE, SAGA_EDTYPE, SAGA_ENOMEM, SAGA_ECUDA, SAGA_EUNSUPPORTED, \
     SAGA_EINTERNAL = range(9)
 SAGA_F32, SAGA_BF16 = 0, 1
-SAGA_GCN, SAGA_SAGE, SAGA_GAT, SAGA_GATED, SAGA_RGCN, SAGA_SAGE_LSTM = 0, 1, 2, 3, 4, 5
+SAGA_GCN, SAGA_SAGE, SAGA_GAT, SAGA_GATED, SAGA_RGCN, SAGA_SAGE_LSTM, SAGA_GGNN = 0, 1, 2, 3, 4, 5, 6
+SAGA_AGG_SUM, SAGA_AGG_MAX = 0, 1
 SAGA_ACT_NONE, SAGA_ACT_RELU, SAGA_ACT_ELU = 0, 1, 2
 MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GATED, "rgcn": SAGA_RGCN,
-          "sage_lstm": SAGA_SAGE_LSTM}
+          "sage_lstm": SAGA_SAGE_LSTM, "ggnn": SAGA_GGNN}
 
 # Every symbol include/saga.h declares (checked by tests/test_abi.py).
 EXPORTS = ["saga_abi_version", "saga_graph_build", "saga_graph_info", "saga_graph_copy_csr",
@@ -48,7 +49,8 @@ class saga_tensor(ctypes.Structure):
 
 class saga_layer_opts(ctypes.Structure):
     _fields_ = [("in_dim", ctypes.c_int32), ("out_dim", ctypes.c_int32), ("heads", ctypes.c_int32),
-                ("head_dim", ctypes.c_int32), ("act", ctypes.c_int32), ("leaky_slope", ctypes.c_float)]
+                ("head_dim", ctypes.c_int32), ("act", ctypes.c_int32), ("leaky_slope", ctypes.c_float),
+                ("aggregator", ctypes.c_int32)]
 
 
 class saga_weights(ctypes.Structure):
@@ -205,8 +207,9 @@ def saga_free(g: Graph):
     _lib.saga_free(g.handle)
 
 
-def make_opts(in_dim, out_dim, act, heads=0, head_dim=0, leaky_slope=0.2) -> saga_layer_opts:
-    return saga_layer_opts(int(in_dim), int(out_dim), int(heads), int(head_dim), int(act), float(leaky_slope))
+def make_opts(in_dim, out_dim, act, heads=0, head_dim=0, leaky_slope=0.2, aggregator=0) -> saga_layer_opts:
+    return saga_layer_opts(int(in_dim), int(out_dim), int(heads), int(head_dim), int(act), float(leaky_slope),
+                           int(aggregator))
 
 
 def saga_layer_workspace_bytes(kind, g: Graph, opts: saga_layer_opts) -> int:
@@ -233,9 +236,11 @@ def saga_layer(kind, g: Graph, features, weights: dict, out, opts: saga_layer_op
 class Layer:
     """Plans one layer once (opts, workspace) and runs it many times."""
 
-    def __init__(self, kind, g: Graph, in_dim, out_dim, act, dtype, heads=0, head_dim=0, leaky_slope=0.2):
+    def __init__(self, kind, g: Graph, in_dim, out_dim, act, dtype, heads=0, head_dim=0, leaky_slope=0.2,
+                 aggregator=0):
         self.kind, self.g = MODELS.get(kind, kind), g
-        self.opts = make_opts(in_dim, out_dim, act, heads, head_dim, leaky_slope)
+        self.opts = make_opts(in_dim, out_dim, act, heads, head_dim, leaky_slope,
+                              {"sum": 0, "max": 1}.get(aggregator, aggregator))
         nbytes = saga_layer_workspace_bytes(self.kind, g, self.opts)
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
         self.out_shape = (g.num_vertices, out_dim)

@@ -380,6 +380,77 @@ struct SumF32Op {
     }
 };
 
+// NEXT-4 paper-form GGNN (reading A26): per in-edge u -> v the message
+// act([H[u] || H[v]] . W_e + b_e) = act(A[u] + B[v]) by linearity, with A =
+// H W_a and B = H W_b + b_e from one node-level GEMM (AB [n][2f], f = 128);
+// the lane's 4-column slice of B[v] is loaded once per row (begin_row).
+// Sum (fp64 accumulation, as SumF32Op) or elementwise max (exact; -inf
+// marks "no edge yet", 0 for a vertex without in-edges).
+template <bool kMax, bool kRelu>
+struct EdgeMlpOp {
+    static constexpr int kWin = 0;
+    static constexpr int kSlot = 2 * 32 * 4;  // doubles as float pairs
+    __device__ static int win_col(int) { return 0; }
+    struct Acc { double a[4]; float4 b; };
+    struct Val { float4 x; };
+    const float *AB;  // [n][256]
+    float *m;         // [n][128]
+    __device__ __forceinline__ float row_value(int32_t, int) const { return 0.0f; }
+    __device__ __forceinline__ void zero(Acc &c) const {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.a[i] = kMax ? -INFINITY : 0.0;
+    }
+    __device__ __forceinline__ void begin_row(Acc &c, int32_t v, int lane) const {
+        c.b = __ldg(reinterpret_cast<const float4 *>(
+            ptx::mad_wide((uint32_t)v, 1024u, reinterpret_cast<const char *>(AB) + 512 + lane * 16)));
+    }
+    __device__ __forceinline__ Val load(int32_t u, int lane) const {
+        return Val{__ldg(reinterpret_cast<const float4 *>(
+            ptx::mad_wide((uint32_t)u, 1024u, reinterpret_cast<const char *>(AB) + lane * 16)))};
+    }
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float) const {
+        float y[4] = {v.x.x + c.b.x, v.x.y + c.b.y, v.x.z + c.b.z, v.x.w + c.b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (kRelu) y[i] = fmaxf(y[i], 0.0f);
+            if (kMax)
+                c.a[i] = fmax(c.a[i], (double)y[i]);
+            else
+                c.a[i] += (double)y[i];
+        }
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = (kMax && c.a[i] == -INFINITY) ? 0.0f : (float)c.a[i];
+        reinterpret_cast<float4 *>(m + (int64_t)v * 128)[lane] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
+        double2 *d = reinterpret_cast<double2 *>(slot) + lane * 2;
+        d[0] = make_double2(c.a[0], c.a[1]);
+        d[1] = make_double2(c.a[2], c.a[3]);
+    }
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
+        const double2 *d = reinterpret_cast<const double2 *>(slot) + lane * 2;
+        const double2 x = __ldcg(d), y = __ldcg(d + 1);
+        const double p[4] = {x.x, x.y, y.x, y.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.a[i] = kMax ? fmax(c.a[i], p[i]) : c.a[i] + p[i];
+    }
+};
+
+// Ops that carry per-row state loaded at the row's start implement begin_row.
+template <typename Op, typename = void>
+struct has_begin_row { static constexpr bool value = false; };
+template <typename Op>
+struct has_begin_row<Op, decltype(void(&Op::begin_row))> { static constexpr bool value = true; };
+template <typename Op>
+__device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, int32_t v, int32_t n, int lane) {
+    if constexpr (has_begin_row<Op>::value) {
+        if (v < n) op.begin_row(c, v, lane);
+    }
+}
+
 // Ops whose epilogue needs the whole warp (the fused GEMV) implement finish_w.
 template <typename Op>
 __device__ __forceinline__ auto do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int lane,
@@ -482,6 +553,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
 
     typename Op::Acc acc;
     op.zero(acc);
+    begin_row_of(op, acc, v, g.n, lane);
 
     // finish row v (or save its partial if it is the head row), advance to v+1
     auto flush = [&]() {
@@ -501,6 +573,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         row_end = VW.re[v - wr];
         if (kWin) rs = VW.rv[(v - wr) * kWinD + Op::win_col(lane)];
         op.zero(acc);
+        begin_row_of(op, acc, v, g.n, lane);
     };
 
     auto load_cs = [&](int32_t base) -> int32_t {
@@ -614,7 +687,8 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
         case SAGA_SAGE: return (size_t)(width > 32 ? width : 32);
         case SAGA_GAT: return 128;                                // 32 lanes x (m, l, a0, a1)
         case SAGA_GATED:
-        case SAGA_RGCN: return (size_t)2 * 128;                   // 32 lanes x 4 fp64
+        case SAGA_RGCN:
+        case SAGA_GGNN: return (size_t)2 * 128;                   // 32 lanes x 4 fp64
     }
     return 0;
 }
@@ -655,6 +729,17 @@ cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, f
     // U = 4 at 64 registers: measured 3-4% faster than U = 8 (C4, C6), and
     // U = 8 needs more registers (spills at 64, 15% slower at 3 blocks/SM)
     return run<4, 4>(gv, op, ws, st);
+}
+
+cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t f, bool relu, bool max, float *m,
+                                    AggWorkspace ws, cudaStream_t st) {
+    if (f != 128) return cudaErrorInvalidValue;
+    if (max) {
+        if (relu) return run<4, 4>(view(g), EdgeMlpOp<true, true>{AB, m}, ws, st);
+        return run<4, 4>(view(g), EdgeMlpOp<true, false>{AB, m}, ws, st);
+    }
+    if (relu) return run<4, 4>(view(g), EdgeMlpOp<false, true>{AB, m}, ws, st);
+    return run<4, 4>(view(g), EdgeMlpOp<false, false>{AB, m}, ws, st);
 }
 
 }  // namespace saga

@@ -306,6 +306,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   messages: Bm[n][k] = W_type[k / f][k % f][n]             (N = f, K = T f)
 //   gates:    Bg[c][k], c = 256 nt + 64 s + j (unit 64 nt + j; slot s = gin, r, z, ghn),
 //             k < f from W_ih, k >= f from W_hh; gin has no h rows, ghn no m rows.
+// Gate B^T element (c, k) of the GRU GEMM over [m || h] (layout above).
+__device__ __forceinline__ float gru_bt(int f, const float *__restrict__ W_ih, const float *__restrict__ W_hh, int idx) {
+    const int c = idx / (2 * f), k = idx % (2 * f);
+    const int nt = c / 256, slot = (c % 256) / 64, j = nt * 64 + c % 64;
+    const bool from_m = k < f;
+    const int kk = from_m ? k : k - f;
+    if (slot == 1 || slot == 2)  // r (gate 0), z (gate 1)
+        return (from_m ? W_ih : W_hh)[((int64_t)(slot - 1) * f + kk) * f + j];
+    if (slot == 0)               // gin: m rows only
+        return from_m ? W_ih[((int64_t)2 * f + kk) * f + j] : 0.0f;
+    return from_m ? 0.0f : W_hh[((int64_t)2 * f + kk) * f + j];  // ghn: h rows only
+}
+
 __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_ih,
                                 const float *__restrict__ W_hh, float *bm_hi, float *bm_lo, float *bg_hi,
                                 float *bg_lo) {
@@ -320,16 +333,37 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
             hi = bm_hi; lo = bm_lo; idx = i;
         } else {
             idx = i - nm;
-            const int c = idx / (2 * f), k = idx % (2 * f);
-            const int nt = c / 256, slot = (c % 256) / 64, j = nt * 64 + c % 64;
-            const bool from_m = k < f;
-            const int kk = from_m ? k : k - f;
-            if (slot == 1 || slot == 2)  // r (gate 0), z (gate 1)
-                x = (from_m ? W_ih : W_hh)[((int64_t)(slot - 1) * f + kk) * f + j];
-            else if (slot == 0)          // gin: m rows only
-                x = from_m ? W_ih[((int64_t)2 * f + kk) * f + j] : 0.0f;
-            else                         // ghn: h rows only
-                x = from_m ? 0.0f : W_hh[((int64_t)2 * f + kk) * f + j];
+            x = gru_bt(f, W_ih, W_hh, idx);
+            hi = bg_hi; lo = bg_lo;
+        }
+        const float h = tf32_rna(x);
+        hi[idx] = h;
+        lo[idx] = tf32_rna(x - h);
+    }
+}
+
+// GGNN (NEXT-4): edge-MLP B^T [2f][f] (rows c < f: W_a = W_e[0:f] columns, c >= f:
+// W_b = W_e[f:2f] columns), its bias vector [0 | b_e], and the GRU B^T.
+__global__ void k_split_ggnn(int f, const float *__restrict__ W_e, const float *__restrict__ b_e,
+                             const float *__restrict__ W_ih, const float *__restrict__ W_hh, float *be_hi,
+                             float *be_lo, float *bias2, float *bg_hi, float *bg_lo) {
+    const int ne = 2 * f * f, ng = 4 * f * 2 * f;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ne + ng + 2 * f; i += gridDim.x * blockDim.x) {
+        if (i >= ne + ng) {
+            const int c = i - ne - ng;
+            bias2[c] = (c < f || !b_e) ? 0.0f : b_e[c - f];
+            continue;
+        }
+        float x;
+        float *hi, *lo;
+        int idx;
+        if (i < ne) {
+            const int c = i / f, k = i % f;
+            x = W_e[((int64_t)(c < f ? 0 : f) + k) * f + c % f];
+            hi = be_hi; lo = be_lo; idx = i;
+        } else {
+            idx = i - ne;
+            x = gru_bt(f, W_ih, W_hh, idx);
             hi = bg_hi; lo = bg_lo;
         }
         const float h = tf32_rna(x);
@@ -456,6 +490,46 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
     GruEpi none{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
     e = launch_tf32split<128, EPI_MSG>(aS, aS, bmh, bml, M, T * f / kBK, T * f / kBK, 1, m_ws, f, none, st);
     if (e) return e;
+    GruEpi gru{H, b_ih, b_hh, out, nullptr, 0};
+    return launch_tf32split<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
+}
+
+size_t ggnn_tc_workspace_floats(int32_t f) { return (size_t)2 * 2 * f * f + 2 * f + (size_t)2 * 4 * f * 2 * f; }
+
+cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e,
+                                const float *W_ih, const float *W_hh, float *wsplit, float *AB, cudaStream_t st,
+                                const char **why) {
+    if (M == 0) return cudaSuccess;
+    if (f != 128) {
+        *why = "tensor-core GGNN path needs f = 128";
+        return cudaErrorInvalidValue;
+    }
+    float *be_hi = wsplit, *be_lo = be_hi + (size_t)2 * f * f, *bias2 = be_lo + (size_t)2 * f * f;
+    float *bg_hi = bias2 + 2 * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
+    k_split_ggnn<<<256, 256, 0, st>>>(f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
+    cudaError_t e = cudaGetLastError();
+    if (e) return e;
+    CUtensorMap aH, bh, bl;
+    if (!make_map_f32(&aH, H, M, f, f, kBM) || !make_map_f32(&bh, be_hi, 2 * f, f, f, 128) ||
+        !make_map_f32(&bl, be_lo, 2 * f, f, f, 128)) {
+        *why = "cuTensorMapEncodeTiled failed";
+        return cudaErrorInvalidValue;
+    }
+    // AB = H . [W_a | W_b] + [0 | b_e]: two 128-column tiles
+    GruEpi epi{nullptr, nullptr, nullptr, nullptr, bias2, 0};
+    return launch_tf32split<128, EPI_MSG>(aH, aH, bh, bl, M, f / kBK, f / kBK, 2, AB, 2 * f, epi, st);
+}
+
+cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float *H, const float *b_ih,
+                               const float *b_hh, const float *wsplit, float *out, cudaStream_t st, const char **why) {
+    if (M == 0) return cudaSuccess;
+    const float *bg_hi = wsplit + (size_t)2 * 2 * f * f + 2 * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
+    CUtensorMap aM, aH, bgh, bgl;
+    if (!make_map_f32(&aM, m, M, f, f, kBM) || !make_map_f32(&aH, H, M, f, f, kBM) ||
+        !make_map_f32(&bgh, bg_hi, 4 * f, 2 * f, 2 * f, 256) || !make_map_f32(&bgl, bg_lo, 4 * f, 2 * f, 2 * f, 256)) {
+        *why = "cuTensorMapEncodeTiled failed";
+        return cudaErrorInvalidValue;
+    }
     GruEpi gru{H, b_ih, b_hh, out, nullptr, 0};
     return launch_tf32split<256, EPI_GRU>(aM, aH, bgh, bgl, M, 2 * f / kBK, f / kBK, 2, nullptr, 0, gru, st);
 }

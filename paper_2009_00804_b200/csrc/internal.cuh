@@ -102,6 +102,17 @@ cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, 
                                float *m_ws, float *out, cudaStream_t st);
 
 // split-TF32 (4 MMAs per product) tcgen05 GEMMs (gemm_tf32split.cu), config C4.
+// GGNN (NEXT-4): AB = H . [W_a | W_b] + [0 | b_e] (split-TF32, also splits the
+// GRU weights into wsplit), the edge-MLP gather m = sum|max act(A[u] + B[v]),
+// and the GRU GEMM over [m || h].
+size_t ggnn_tc_workspace_floats(int32_t f);
+cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e,
+                                const float *W_ih, const float *W_hh, float *wsplit, float *AB, cudaStream_t st,
+                                const char **why);
+cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t f, bool relu, bool max, float *m,
+                                    AggWorkspace ws, cudaStream_t st);
+cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float *H, const float *b_ih,
+                               const float *b_hh, const float *wsplit, float *out, cudaStream_t st, const char **why);
 size_t gated_tc_workspace_floats(int32_t f, int32_t T);
 cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,

@@ -130,6 +130,7 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GATED: width = (size_t)o.in_dim; break;
         case SAGA_RGCN: width = (size_t)o.in_dim; break;
         case SAGA_SAGE_LSTM: width = (size_t)o.in_dim; break;
+        case SAGA_GGNN: width = (size_t)o.in_dim; break;
     }
     size_t pf = saga::agg_partial_floats(kind, (int32_t)width, 8);
     if (kind == SAGA_GCN) pf = (size_t)2 * std::max({o.in_dim, o.out_dim, 32});  // fp64 partials on the fp32 path
@@ -153,6 +154,11 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
             p.inter0 = align_up((size_t)2 * 4 * n * (size_t)std::max(o.in_dim, 0));             // P = X W_ih, bf16
             p.inter1 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0));                 // h (LSTM out), bf16
             p.inter2 = align_up(saga::lstm_workspace_bytes());                                  // staged W_hh^T
+            break;
+        case SAGA_GGNN:
+            p.inter0 = align_up(sizeof(float) * n * 2 * (size_t)std::max(o.in_dim, 0));        // AB = [A | B]
+            p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
+            p.inter2 = align_up(sizeof(float) * saga::ggnn_tc_workspace_floats(128));           // split W_e, GRU
             break;
         case SAGA_RGCN:
             p.inter0 = align_up(sizeof(float) * n * (size_t)g.num_etypes * (size_t)std::max(o.in_dim, 0));  // S (type means)
@@ -237,7 +243,7 @@ saga_status saga_graph_copy_csr(const saga_graph *g, int64_t *row_ptr, int32_t *
 saga_status saga_layer_workspace_bytes(saga_model kind, const saga_graph *g, const saga_layer_opts *opts,
                                        size_t *bytes) {
     if (!g || !opts || !bytes) return fail(SAGA_EINVAL, "NULL argument");
-    if (kind < SAGA_GCN || kind > SAGA_SAGE_LSTM) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+    if (kind < SAGA_GCN || kind > SAGA_GGNN) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
     *bytes = plan_for(kind, g->d, *opts).total;
     return SAGA_OK;
 }
@@ -479,6 +485,38 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 e = launch_gemm_bf16_tc(a, st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "sage_lstm gemm: %s (%s)", cudaGetErrorString(e), why);
+            return SAGA_OK;
+        }
+        case SAGA_GGNN: {
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GGNN supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GGNN supports in=out=128");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GGNN act must be NONE/RELU");
+            if (o.aggregator != SAGA_AGG_SUM && o.aggregator != SAGA_AGG_MAX)
+                return fail(SAGA_EUNSUPPORTED, "GGNN aggregator must be SUM or MAX");
+            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "GGNN needs W (edge MLP), W_ih, W_hh, b_ih, b_hh");
+            const float *H = static_cast<const float *>(x->data);
+            float *AB = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
+            float *wsplit = reinterpret_cast<float *>(i2);
+            {
+                ProfScope ps_("ggnn_edge_tf32x3", st);
+                e = launch_ggnn_edge_tc(d.n, o.in_dim, H, static_cast<const float *>(w->W), w->bias,
+                                        static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
+                                        wsplit, AB, st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "ggnn edge gemm: %s (%s)", cudaGetErrorString(e), why);
+            {
+                ProfScope ps_("agg_edge_mlp_f32", st);
+                e = launch_agg_edge_mlp_f32(d, AB, o.in_dim, o.act == SAGA_ACT_RELU, o.aggregator == SAGA_AGG_MAX, m,
+                                            aw, st);
+            }
+            if (e) return cuda_fail(e, "ggnn edge-mlp gather");
+            {
+                ProfScope ps_("ggnn_gru_tf32x3", st);
+                e = launch_ggnn_gru_tc(d.n, o.in_dim, m, H, w->b_ih, w->b_hh, wsplit, static_cast<float *>(out->data),
+                                       st, &why);
+            }
+            if (e) return fail(SAGA_ECUDA, "ggnn gru: %s (%s)", cudaGetErrorString(e), why);
             return SAGA_OK;
         }
         case SAGA_RGCN: {

@@ -25,6 +25,8 @@ LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)
     "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C6": [("SumF32Op", "agg_typed_mean_f32"), ("TypedF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3")],
     "C7": [("k_lstm_gather", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
+    "C8": [("EdgeMlpOp", "agg_edge_mlp_f32"), ("k_gemm_tf32split<256", "ggnn_gru_tf32x3"),
+           ("k_gemm_tf32split<128", "ggnn_edge_tf32x3")],
 }
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram_read"),
         ("dram__bytes_write.sum", "dram_write"), ("lts__t_sector_hit_rate.pct", "L2_hit_%"),
@@ -83,7 +85,7 @@ def main(tag):
     traffic_path = os.path.join(dst, "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     md = [f"# ncu summary `{tag}` (ncu --set full --clock-control none; cold-cache replays)\n"]
-    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7"]:
+    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"]:
         rep = os.path.join(src, f"full_{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -125,7 +127,7 @@ def main(tag):
         for k, (n, t) in sorted(ours.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"{k},{n},{t:.4f},{t / tot:.4f}")
         open(os.path.join(dst, f"{tag}_launch_shares_C5.csv"), "w").write("\n".join(lines) + "\n")
-    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7"]:
+    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"]:
         b = os.path.join(src, f"bench_{cfg}.json")
         if os.path.exists(b):
             shutil.copy(b, os.path.join(dst, f"{tag}_bench_{cfg}.json"))

@@ -50,6 +50,13 @@ def gpu_step(saga, cfg, g, d, layers=None):
         w = {k: d[k].contiguous() for k in ("W", "W_ih", "W_hh", "b_ih", "b_hh")}
         w["bias"] = d["b"]
         return [lay(d["X"], w)], [lay]
+    if cfg.model == "ggnn":
+        f = cfg.dims[0]
+        lay = layers[0] if layers else saga.Layer("ggnn", g, f, f, act_relu, dt,
+                                                  aggregator=cfg.extra.get("agg", "sum"))
+        w = {k: d[k].contiguous() for k in ("W_ih", "W_hh", "b_ih", "b_hh")}
+        w["W"], w["bias"] = d["W_e"].contiguous(), d["b_e"]
+        return [lay(d["H"], w)], [lay]
     if cfg.model == "rgcn":
         f, fo = cfg.dims
         lay = layers[0] if layers else saga.Layer("rgcn", g, f, fo, act_relu, dt)
@@ -82,6 +89,9 @@ def oracle_step(oracle, cfg, og, d, rows=None, layer_inputs=None):
         return [oracle.gated(og, c["H"], c["W_type"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], rows=rows)]
     if cfg.model == "rgcn":
         return [oracle.rgcn(og, c["H"], c["W_type"], c["W_self"], c["b"], act=1, rows=rows)]
+    if cfg.model == "ggnn":
+        return [oracle.ggnn(og, c["H"], c["W_e"], c["b_e"], c["W_ih"], c["W_hh"], c["b_ih"], c["b_hh"], act=1,
+                            agg=cfg.extra.get("agg", "sum"), rows=rows)]
     if cfg.model == "sage_lstm":
         return [oracle.sage_lstm(og, c["X"], c["W_ih"].float(), c["W_hh"].float(), c["b_ih"], c["b_hh"],
                                  c["W"].float(), c["b"], act=1, rows=rows)]

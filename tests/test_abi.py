@@ -43,14 +43,31 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_error_string(lib):
-    assert lib.saga_abi_version() == 1
+    assert lib.saga_abi_version() == 2
     assert isinstance(lib.saga_last_error(), str)
 
 
-def test_struct_layouts_match_header(lib):
-    assert ctypes.sizeof(lib.saga_tensor) == 32
-    assert ctypes.sizeof(lib.saga_layer_opts) == 24
-    assert ctypes.sizeof(lib.saga_weights) == 9 * 8
+def test_struct_layouts_match_header(lib, tmp_path):
+    """ctypes mirrors vs the C compiler's view of include/saga.h (size and
+    every field offset), so a header change cannot drift from the binding."""
+    fields = {"saga_tensor": lib.saga_tensor, "saga_layer_opts": lib.saga_layer_opts,
+              "saga_weights": lib.saga_weights}
+    lines = []
+    for name, cls in fields.items():
+        lines.append(f'printf("%zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({name}, {fname}));')
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "saga.h"\nint main(void) {\n'
+                   + "\n".join(lines) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    want = []
+    for cls in fields.values():
+        want.append(ctypes.sizeof(cls))
+        want.extend(getattr(cls, f).offset for f, _ in cls._fields_)
+    assert got == want
 
 
 def test_product_package_has_no_oracle_or_fallback():

@@ -145,3 +145,33 @@ def test_gated_etype_out_of_range(saga):
     with pytest.raises(saga.SagaError) as ei:
         _graph(saga, 4, [0, 1, 2, 3], [1, 2, 3, 0], [0, 3, 4, 1], 4)
     assert ei.value.status == saga.SAGA_ERANGE and ei.value.first_bad_edge == 2
+
+
+@pytest.mark.gpu
+def test_ggnn_rejects_bad_arguments(saga):
+    g = _graph(saga, 4, [0, 1, 2, 3], [1, 2, 3, 0])
+    dev = "cuda"
+    h = torch.randn(4, 128, device=dev)
+    w = {"W": torch.randn(256, 128, device=dev), "W_ih": torch.randn(3, 128, 128, device=dev),
+         "W_hh": torch.randn(3, 128, 128, device=dev), "b_ih": torch.randn(3, 128, device=dev),
+         "b_hh": torch.randn(3, 128, device=dev)}
+    out = torch.empty(4, 128, device=dev)
+
+    def status(opts, ww=w, x=h, o=out):
+        ws = torch.empty(saga.saga_layer_workspace_bytes(saga.SAGA_GGNN, g, opts), dtype=torch.uint8, device=dev)
+        with pytest.raises(saga.SagaError) as ei:
+            saga.saga_layer(saga.SAGA_GGNN, g, x, ww, o, opts, ws)
+        return ei.value.status
+
+    assert status(saga.make_opts(128, 128, saga.SAGA_ACT_RELU, aggregator=7)) == saga.SAGA_EUNSUPPORTED
+    assert status(saga.make_opts(128, 128, saga.SAGA_ACT_ELU)) == saga.SAGA_EUNSUPPORTED
+    assert status(saga.make_opts(128, 128, saga.SAGA_ACT_RELU), ww={k: v for k, v in w.items() if k != "W"}) == \
+        saga.SAGA_EINVAL
+    assert status(saga.make_opts(128, 128, saga.SAGA_ACT_RELU), x=h.bfloat16(), o=out.bfloat16()) == \
+        saga.SAGA_EDTYPE
+    # a valid call (bias omitted = 0) still works afterwards
+    opts = saga.make_opts(128, 128, saga.SAGA_ACT_RELU, aggregator=saga.SAGA_AGG_MAX)
+    ws = torch.empty(saga.saga_layer_workspace_bytes(saga.SAGA_GGNN, g, opts), dtype=torch.uint8, device=dev)
+    saga.saga_layer(saga.SAGA_GGNN, g, h, w, out, opts, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()

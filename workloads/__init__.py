@@ -29,7 +29,7 @@ SEED_ROOT = 200900804  # arXiv id, SURVEY.md 8(d) "Seeds"
 @dataclass(frozen=True)
 class Config:
     name: str
-    model: str              # "gcn" | "sage" | "gat" | "gated"
+    model: str              # "gcn" | "sage" | "gat" | "gated" | "rgcn" | "sage_lstm" | "ggnn"
     graph: str              # "er" | "rmat"
     n: int                  # vertices
     m: int                  # generated edges (before appended self-loops)
@@ -51,7 +51,8 @@ class Config:
     def f_canon(self) -> int:
         """Row width Gather reduces in SAGA order (reading A20)."""
         return {"gcn": self.dims[0], "sage": self.dims[0], "gat": self.dims[-1],
-                "gated": self.dims[0], "rgcn": self.dims[0], "sage_lstm": self.dims[0]}[self.model]
+                "gated": self.dims[0], "rgcn": self.dims[0], "sage_lstm": self.dims[0],
+                "ggnn": self.dims[0]}[self.model]
 
     def updates_per_layer(self) -> int:
         """Edge-feature updates of one layer = E * F_canon (reading A20).
@@ -85,6 +86,10 @@ CONFIGS = {
     # SURVEY 8(f) NEXT-2 (not a BASELINE config): GraphSAGE-LSTM on C2's graph recipe,
     # bf16 128 -> 128, LSTM hidden 128, ReLU
     "C7": Config("C7", "sage_lstm", "rmat", 1 << 16, 1 << 20, False, True, "bf16", (128, 128), index=7),
+    # SURVEY 8(f) NEXT-4 (not a BASELINE config): paper-form GGNN (edge MLP on
+    # [h_src || h_dst] + ReLU, sum gather, GRU) on C4's graph shape, fp32 128
+    "C8": Config("C8", "ggnn", "rmat", 1 << 17, 1 << 21, False, False, "f32", (128, 128), index=8,
+                 extra={"agg": "sum"}),
 }
 
 
@@ -349,6 +354,16 @@ def make_inputs(cfg: Config, device="cpu", graph=True):
         d["W_type"] = uniform(k, "W_type", T * f, fo, bnd, device).view(T, f, fo)
         d["W_self"] = uniform(k, "W_self", f, fo, bnd, device)
         d["b"] = uniform(k, "b", 1, fo, bnd, device).view(fo)
+    elif cfg.model == "ggnn":
+        f, _ = cfg.dims
+        bnd_e, bnd = 1.0 / math.sqrt(2 * f), 1.0 / math.sqrt(f)
+        d["H"] = normal(k, f"H/{n}", n, f, 1.0, device)
+        d["W_e"] = uniform(k, "W_e", 2 * f, f, bnd_e, device)          # [src rows; dst rows] x out
+        d["b_e"] = uniform(k, "b_e", 1, f, bnd_e, device).view(f)
+        d["W_ih"] = uniform(k, "W_ih", 3 * f, f, bnd, device).view(3, f, f)
+        d["W_hh"] = uniform(k, "W_hh", 3 * f, f, bnd, device).view(3, f, f)
+        d["b_ih"] = uniform(k, "b_ih", 3, f, bnd, device)
+        d["b_hh"] = uniform(k, "b_hh", 3, f, bnd, device)
     else:
         raise ValueError(cfg.model)
     return d
