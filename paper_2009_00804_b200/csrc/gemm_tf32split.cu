@@ -20,7 +20,7 @@
 // |S| ~ 130 (tests/test_gpu_parity.py zoo "hub70k"); the fp32 FFMA reference
 // kernels give 2.0e-5 there.
 //
-// Kernel (persistent, one CTA per SM, 320 threads):
+// Kernel (persistent, one CTA per SM, 448 threads):
 //   warp 0      TMA producer: per 32-wide K block, the fp32 A tile (128 rows,
 //               128-byte swizzle; A may come from two tensors along K) and the
 //               pre-split B_hi / B_lo tiles (BN rows of W^T),
@@ -28,7 +28,11 @@
 //               (M = 128, N = BN, K = 8): 3 MMAs per K step,
 //   warps 2..5  converters: A tile -> A_hi (in place) + A_lo (elementwise,
 //               so the swizzled layout is preserved), fence.proxy.async,
-//   warps 6..9  epilogue: tcgen05.ld, then store (messages) or the GRU.
+//   warps 6..13 epilogue: tcgen05.ld, then store (messages) or the GRU; two
+//               warps per TMEM lane quarter, each half of the tile's columns
+//               (with one warp per quarter the GRU epilogue's dependent
+//               activations were the kernel's bound: 0.21 ms of 0.29 with
+//               every load, conversion and MMA switched off).
 // The accumulator is double-buffered in TMEM (2 x BN columns) so the
 // epilogue of one tile overlaps the MMAs of the next.
 #include <cuda.h>
@@ -43,7 +47,8 @@
 namespace saga {
 namespace {
 
-constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;                // two per TMEM lane quarter, each half the columns
+constexpr int kThreads = 192 + 32 * kEpiWarps;
 constexpr int kBM = 128;
 constexpr int kBK = 32;                     // fp32 per 128-byte swizzle row
 constexpr int kATile = kBM * kBK * 4;       // 16 KB
@@ -80,7 +85,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// sigma(x) = 1 / (1 + e^-x) with the approximate reciprocal, tanh(x) = 2 sigma(2x) - 1:
+// |error| ~1e-7 absolute.  The GRU epilogue applies them to every gate output
+// of every row; with IEEE division and tanhf it was the kernel's bound.
+__device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanhf_(float x) { return 2.0f * sigmoidf_(2.0f * x) - 1.0f; }
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -108,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&bar->tfull[a], 1);
-            ptx::mbar_init(&bar->tempty[a], 128);
+            ptx::mbar_init(&bar->tempty[a], 32 * kEpiWarps);
         }
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmA0);
@@ -220,7 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ============================ epilogue ================================
+        // warps 6 .. 6 + kEpiWarps - 1: TMEM lane quarter q = warp % 4, column half
         const int q = warp & 3;       // TMEM lane quarter this warp may access
+        const int half = (warp - 6) >> 2;
         const int r = q * 32 + lane;  // row within the tile
         int it = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
             if (EPI == EPI_MSG) {
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = half; c < BN / 32; c += 2) {
                     uint32_t v[32];
                     ptx::tmem_ld32(tbase + c * 32, v);
                     ptx::tmem_ld_wait();
@@ -251,39 +262,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt)
+                // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt); this warp: 32 units, 16 at a time
 #pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t vr[32], vz[32];
-                    ptx::tmem_ld32(tbase + 64 + c * 32, vr);
-                    ptx::tmem_ld32(tbase + 128 + c * 32, vz);
-                    ptx::tmem_ld_wait();
-                    const int j0 = nt * 64 + c * 32;
-                    float rg[32], zg[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        rg[j] = sigmoidf_(__uint_as_float(vr[j]) + __ldg(gru.b_ih + j0 + j) + __ldg(gru.b_hh + j0 + j));
-                        zg[j] = sigmoidf_(__uint_as_float(vz[j]) + __ldg(gru.b_ih + 128 + j0 + j) +
-                                          __ldg(gru.b_hh + 128 + j0 + j));
-                    }
-                    uint32_t vi[32], vh[32];
-                    ptx::tmem_ld32(tbase + c * 32, vi);
-                    ptx::tmem_ld32(tbase + 192 + c * 32, vh);
+                for (int c = 2 * half; c < 2 * half + 2; ++c) {
+                    uint32_t vr[16], vz[16], vi[16], vh[16];
+                    ptx::tmem_ld16(tbase + 64 + c * 16, vr);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, vz);
+                    ptx::tmem_ld16(tbase + c * 16, vi);
+                    ptx::tmem_ld16(tbase + 192 + c * 16, vh);
                     ptx::tmem_ld_wait();
                     if (row < M) {
+                        const int j0 = nt * 64 + c * 16;
                         const float4 *hp = reinterpret_cast<const float4 *>(gru.h + row * 128 + j0);
                         float4 *op = reinterpret_cast<float4 *>(gru.out + row * 128 + j0);
 #pragma unroll
-                        for (int j4 = 0; j4 < 8; ++j4) {
+                        for (int j4 = 0; j4 < 4; ++j4) {
                             const float4 hv = __ldg(hp + j4);
                             const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
                             float o[4];
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const int j = 4 * j4 + e;
-                                const float n = tanhf(__uint_as_float(vi[j]) + __ldg(gru.b_ih + 256 + j0 + j) +
-                                                      rg[j] * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
-                                o[e] = (1.0f - zg[j]) * n + zg[j] * hh[e];
+                                const float rg = sigmoidf_(__uint_as_float(vr[j]) + __ldg(gru.b_ih + j0 + j) +
+                                                           __ldg(gru.b_hh + j0 + j));
+                                const float zg = sigmoidf_(__uint_as_float(vz[j]) + __ldg(gru.b_ih + 128 + j0 + j) +
+                                                           __ldg(gru.b_hh + 128 + j0 + j));
+                                const float n = tanhf_(__uint_as_float(vi[j]) + __ldg(gru.b_ih + 256 + j0 + j) +
+                                                       rg * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
+                                o[e] = (1.0f - zg) * n + zg * hh[e];
                             }
                             op[j4] = make_float4(o[0], o[1], o[2], o[3]);
                         }
