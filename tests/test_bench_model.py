@@ -3,6 +3,8 @@ the roofline object."""
 import importlib.util
 import os
 
+import numpy as np
+
 import pytest
 
 import workloads as W
@@ -69,3 +71,16 @@ def test_hbm_bound_contraction_is_held_to_hbm(bench):
     assert r["bound"] == "hbm" and r["unit"] == "GB/s"
     c4 = bench.algorithmic(W.CONFIGS["C4"])["gated_apply_tf32x3"]
     assert bench.roofline_of("g", c4, 0.36e-3, pk, None)["bound"] == "tensor"
+
+
+@pytest.mark.parametrize("cfg", sorted(W.CONFIGS))
+def test_cpu_baseline_leg_runs_every_model(bench, cfg):
+    """bench.py's cpu_baseline / --impl reference leg evaluates the oracle for
+    every configured model (tiny scaled graph, CPU only)."""
+    import oracle
+    c = W.scaled(W.CONFIGS[cfg], 64, 256, cfg + "t")
+    d = W.make_inputs(c, "cpu")
+    og = oracle.csr_build(c.n, d["src"], d["dst"], None if d.get("etype") is None else d["etype"], c.num_etypes)
+    rows = np.arange(0, c.n, 7, dtype=np.int64)
+    out = bench.harness_step_rows(c, og, d, rows, oracle)
+    assert np.all(np.isfinite(np.asarray(out)))
