@@ -90,6 +90,7 @@ Prof g_prof;
 // RAII bracket around one kernel launch (no-op unless profiling is on).
 struct ProfScope {
     bool on;
+    unsigned flags = cudaEventRecordDefault;
     ProfRec r{};
     cudaStream_t st;
     ProfScope(const char *name, cudaStream_t s) : on(false), st(s) {
@@ -99,11 +100,16 @@ struct ProfScope {
         r.name = g_prof.id(name);
         r.a = g_prof.get();
         r.b = g_prof.get();
-        cudaEventRecord(r.a, st);
+        // under stream capture the pair must be event-record NODES of the graph
+        // (external); outside capture the flag is an error
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+            flags = cudaEventRecordExternal;
+        cudaEventRecordWithFlags(r.a, st, flags);
     }
     ~ProfScope() {
         if (!on) return;
-        cudaEventRecord(r.b, st);
+        cudaEventRecordWithFlags(r.b, st, flags);
         std::lock_guard<std::mutex> lk(g_prof.mu);
         g_prof.pending.push_back(r);
     }

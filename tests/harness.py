@@ -21,46 +21,50 @@ def gpu_graph(saga, cfg, d):
     return saga.saga_graph_build(cfg.n, d["src"], d["dst"], d.get("etype"), cfg.num_etypes)
 
 
-def gpu_step(saga, cfg, g, d, layers=None):
-    """Run the configured step; returns list of per-layer outputs (device)."""
+def gpu_step(saga, cfg, g, d, layers=None, outs=None):
+    """Run the configured step; returns list of per-layer outputs (device).
+
+    `outs` (the outputs of an earlier call) are reused as output buffers: no
+    allocation, so the step can be captured in a CUDA graph."""
+    o = (lambda i: outs[i]) if outs else (lambda i: None)
     act_relu = saga.SAGA_ACT_RELU
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     if cfg.model == "gcn":
         lay = layers[0] if layers else saga.Layer("gcn", g, cfg.dims[0], cfg.dims[1], act_relu, dt)
-        return [lay(d["X"], {"W": d["W"], "bias": d["b"]})], [lay]
+        return [lay(d["X"], {"W": d["W"], "bias": d["b"]}, out=o(0))], [lay]
     if cfg.model == "sage":
         f0, f1, f2 = cfg.dims
         l1 = layers[0] if layers else saga.Layer("sage", g, f0, f1, act_relu, dt)
         l2 = layers[1] if layers else saga.Layer("sage", g, f1, f2, saga.SAGA_ACT_NONE, dt)
-        h1 = l1(d["X"], {"W": d["W1"]})
-        return [h1, l2(h1, {"W": d["W2"]})], [l1, l2]
+        h1 = l1(d["X"], {"W": d["W1"]}, out=o(0))
+        return [h1, l2(h1, {"W": d["W2"]}, out=o(1))], [l1, l2]
     if cfg.model == "gat":
         fi, fo = cfg.dims
         lay = layers[0] if layers else saga.Layer("gat", g, fi, fo, saga.SAGA_ACT_ELU, dt, heads=cfg.heads,
                                                   head_dim=fo // cfg.heads, leaky_slope=0.2)
-        return [lay(d["X"], {"W": d["W"], "attn_src": d["a_src"], "attn_dst": d["a_dst"]})], [lay]
+        return [lay(d["X"], {"W": d["W"], "attn_src": d["a_src"], "attn_dst": d["a_dst"]}, out=o(0))], [lay]
     if cfg.model == "gated":
         f = cfg.dims[0]
         lay = layers[0] if layers else saga.Layer("gated", g, f, f, saga.SAGA_ACT_NONE, dt)
         w = {k: d[k].contiguous() for k in ("W_type", "W_ih", "W_hh", "b_ih", "b_hh")}
-        return [lay(d["H"], w)], [lay]
+        return [lay(d["H"], w, out=o(0))], [lay]
     if cfg.model == "sage_lstm":
         f, fo = cfg.dims
         lay = layers[0] if layers else saga.Layer("sage_lstm", g, f, fo, act_relu, dt)
         w = {k: d[k].contiguous() for k in ("W", "W_ih", "W_hh", "b_ih", "b_hh")}
         w["bias"] = d["b"]
-        return [lay(d["X"], w)], [lay]
+        return [lay(d["X"], w, out=o(0))], [lay]
     if cfg.model == "ggnn":
         f = cfg.dims[0]
         lay = layers[0] if layers else saga.Layer("ggnn", g, f, f, act_relu, dt,
                                                   aggregator=cfg.extra.get("agg", "sum"))
         w = {k: d[k].contiguous() for k in ("W_ih", "W_hh", "b_ih", "b_hh")}
         w["W"], w["bias"] = d["W_e"].contiguous(), d["b_e"]
-        return [lay(d["H"], w)], [lay]
+        return [lay(d["H"], w, out=o(0))], [lay]
     if cfg.model == "rgcn":
         f, fo = cfg.dims
         lay = layers[0] if layers else saga.Layer("rgcn", g, f, fo, act_relu, dt)
-        return [lay(d["H"], {"W_type": d["W_type"].contiguous(), "W": d["W_self"], "bias": d["b"]})], [lay]
+        return [lay(d["H"], {"W_type": d["W_type"].contiguous(), "W": d["W_self"], "bias": d["b"]}, out=o(0))], [lay]
     raise ValueError(cfg.model)
 
 
