@@ -115,6 +115,22 @@ struct ProfScope {
     }
 };
 
+// The graph arrays and the build's scratch come from the device's default
+// stream-ordered pool.  With the pool's default release threshold (0) every
+// synchronisation -- the build's range check -- hands the memory back to the
+// driver and the next build maps it again; keep up to 4 GiB cached instead
+// (raised once per device, never lowered below a caller's setting).
+void keep_pool_memory() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t cur = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) != cudaSuccess) return;
+    uint64_t want = uint64_t(4) << 30;
+    if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+}
+
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -200,6 +216,7 @@ saga_status saga_graph_build(int32_t num_vertices, int64_t num_edges, const int3
     }
     saga_graph *g = new (std::nothrow) saga_graph();
     if (!g) return fail(SAGA_ENOMEM, "host allocation failed");
+    keep_pool_memory();
     int64_t bad = -1;
     const char *why = "";
     saga_status s = saga::build_graph(num_vertices, num_edges, src, dst, etype, num_etypes,
