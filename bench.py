@@ -130,6 +130,10 @@ def algorithmic(cfg):
         fi, fo = cfg.dims
         out["gcn_f32_fused"] = {"bytes": e * 4 + (n + 1) * 8 + n * fi * 4 + n * 4 + n * fo * 4,
                                 "flops": 2 * e * fi + 2 * n * fi * fo, "peak": "hbm"}
+    elif cfg.model == "sage" and cfg.extra.get("fused"):
+        f0, f1, f2 = cfg.dims   # NEXT-1: per launch x rows + gathered rows + out (mean of the two layers)
+        out["sage_fused_tc"] = {"bytes": (e * 4 + (n + 1) * 8 + n * 4 + n * (f0 + f1) * 2 + n * (f1 + f2) * 2) // 2,
+                                "flops": (e * (f0 + f1) + 2 * n * (2 * f0 * f1 + 2 * f1 * f2)) // 2, "peak": "hbm"}
     elif cfg.model == "sage":
         f0, f1, f2 = cfg.dims   # two layers: agg widths f0, f1; GEMMs 2f0 -> f1, 2f1 -> f2 (mean of the two launches)
         out["agg_mean_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * 4 + n * (f0 + f1) * 2 * 2 // 2,
@@ -332,7 +336,8 @@ def workload_config(cfg):
             "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128",
             "C7": "GraphSAGE-LSTM bf16 (NEXT-2), R-MAT N=2^16 E=2^20 distinct, 128->128",
             "C8": "paper-form GGNN fp32 (NEXT-4: edge MLP on [h_src||h_dst] + ReLU, sum, GRU), R-MAT N=2^17 E=2^21, 128"}
-    return {"workload": f"{cfg.name}: {desc.get(cfg.name, cfg.name)}", "vertices": cfg.n, "edges": cfg.num_edges,
+    w = desc.get(cfg.name, cfg.name) + (" [NEXT-1 fused Gather + concat-GEMM]" if cfg.extra.get("fused") else "")
+    return {"workload": f"{cfg.name}: {w}", "vertices": cfg.n, "edges": cfg.num_edges,
             "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
 
 
@@ -546,6 +551,8 @@ def main():
     ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly (no CUDA graph)")
+    ap.add_argument("--sage-fused", action="store_true",
+                    help="SAGE (C2): Gather fused with the concat-GEMM in one kernel (NEXT-1)")
     ap.add_argument("--ref-edges", type=int, default=2_000_000,
                     help="in-edges per oracle sample (bounded CPU work)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -556,6 +563,11 @@ def main():
     if args.warmup < 3:
         args.warmup = 3   # timing rule: >= 3 warm-up steps
     cfg = W.CONFIGS[args.config]
+    if args.sage_fused:
+        if cfg.model != "sage":
+            raise SystemExit("--sage-fused applies to the SAGE config (C2)")
+        cfg = W.scaled(cfg, cfg.n, cfg.m, cfg.name)
+        cfg.extra["fused"] = True
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

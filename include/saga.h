@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SAGA_ABI_VERSION 2  /* 2: SAGA_GGNN, saga_layer_opts.aggregator */
+#define SAGA_ABI_VERSION 3  /* 2: SAGA_GGNN, saga_layer_opts.aggregator; 3: .fused */
 
 #if defined(__GNUC__)
 #define SAGA_API __attribute__((visibility("default")))
@@ -89,6 +89,9 @@ typedef struct {
                               /* GAT must be ELU; GATED ignores it (GRU)                   */
     float leaky_slope;        /* GAT LeakyReLU negative slope in [0, 1] (0.2 in config C3) */
     int32_t aggregator;       /* saga_aggregator, GGNN only (else ignored)                 */
+    int32_t fused;            /* SAGE only: 1 = Gather and the concat-GEMM as ONE kernel    */
+                              /* (in_dim 128, out_dim 64 or 128), 0 =   */
+                              /* the two-kernel path (default; measured faster at C2)       */
 } saga_layer_opts;
 
 /* Weights (device, row-major, [in][out] orientation = x . W, reading A8).

@@ -50,7 +50,7 @@ class saga_tensor(ctypes.Structure):
 class saga_layer_opts(ctypes.Structure):
     _fields_ = [("in_dim", ctypes.c_int32), ("out_dim", ctypes.c_int32), ("heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("act", ctypes.c_int32), ("leaky_slope", ctypes.c_float),
-                ("aggregator", ctypes.c_int32)]
+                ("aggregator", ctypes.c_int32), ("fused", ctypes.c_int32)]
 
 
 class saga_weights(ctypes.Structure):
@@ -207,9 +207,10 @@ def saga_free(g: Graph):
     _lib.saga_free(g.handle)
 
 
-def make_opts(in_dim, out_dim, act, heads=0, head_dim=0, leaky_slope=0.2, aggregator=0) -> saga_layer_opts:
+def make_opts(in_dim, out_dim, act, heads=0, head_dim=0, leaky_slope=0.2, aggregator=0,
+              fused=0) -> saga_layer_opts:
     return saga_layer_opts(int(in_dim), int(out_dim), int(heads), int(head_dim), int(act), float(leaky_slope),
-                           int(aggregator))
+                           int(aggregator), int(fused))
 
 
 def saga_layer_workspace_bytes(kind, g: Graph, opts: saga_layer_opts) -> int:
@@ -237,10 +238,10 @@ class Layer:
     """Plans one layer once (opts, workspace) and runs it many times."""
 
     def __init__(self, kind, g: Graph, in_dim, out_dim, act, dtype, heads=0, head_dim=0, leaky_slope=0.2,
-                 aggregator=0):
+                 aggregator=0, fused=False):
         self.kind, self.g = MODELS.get(kind, kind), g
         self.opts = make_opts(in_dim, out_dim, act, heads, head_dim, leaky_slope,
-                              {"sum": 0, "max": 1}.get(aggregator, aggregator))
+                              {"sum": 0, "max": 1}.get(aggregator, aggregator), int(fused))
         nbytes = saga_layer_workspace_bytes(self.kind, g, self.opts)
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
         self.out_shape = (g.num_vertices, out_dim)

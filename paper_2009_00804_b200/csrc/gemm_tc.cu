@@ -295,18 +295,6 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// 2-D bf16 row-major [rows][cols] map with a {64 col, 128 row} box, 128B swizzle.
-bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols) {
-    EncodeFn enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, 128};
-    cuuint32_t estr[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 template <int BN>
 cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorMap &mc,
@@ -326,6 +314,19 @@ cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMa
 
 }  // namespace
 
+// 2-D bf16 row-major [rows][cols] map with a {64 col, 128 row} box, 128B swizzle.
+bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char **why) {
     if (a.M == 0) return cudaSuccess;
     const int K = a.K0 + a.K1;
@@ -334,8 +335,8 @@ cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char *
         return cudaErrorInvalidValue;
     }
     CUtensorMap m0, m1, mc;
-    if (!make_map(&m0, a.A0, a.M, a.K0) || !make_map(&m1, a.K1 ? a.A1 : a.A0, a.M, a.K1 ? a.K1 : a.K0) ||
-        !make_map(&mc, a.out, a.M, a.N)) {
+    if (!make_map_bf16(&m0, a.A0, a.M, a.K0) || !make_map_bf16(&m1, a.K1 ? a.A1 : a.A0, a.M, a.K1 ? a.K1 : a.K0) ||
+        !make_map_bf16(&mc, a.out, a.M, a.N)) {
         *why = "cuTensorMapEncodeTiled failed";
         return cudaErrorInvalidValue;
     }

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -105,6 +106,17 @@ cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, 
 // GGNN (NEXT-4): AB = H . [W_a | W_b] + [0 | b_e] (split-TF32, also splits the
 // GRU weights into wsplit), the edge-MLP gather m = sum|max act(A[u] + B[v]),
 // and the GRU GEMM over [m || h].
+// 2-D bf16 row-major [rows][cols] tensor map, {64 col, 128 row} box, 128B swizzle (gemm_tc.cu).
+bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols);
+
+// NEXT-1: GraphSAGE-mean aggregation fused with its tcgen05 concat-GEMM
+// (sage_fused.cu); img = workspace for the staged W^T image.
+bool sage_fused_supported(int32_t in_dim, int32_t out_dim);
+size_t sage_fused_workspace_bytes(int32_t out_dim);
+cudaError_t launch_sage_fused(const GraphDev &g, const __nv_bfloat16 *X, int32_t in_dim, const __nv_bfloat16 *W,
+                              int32_t out_dim, const float *bias, int act, __nv_bfloat16 *out, void *img,
+                              cudaStream_t st, const char **why);
+
 size_t ggnn_tc_workspace_floats(int32_t f);
 cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e,
                                 const float *W_ih, const float *W_hh, float *wsplit, float *AB, cudaStream_t st,

@@ -161,7 +161,10 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
     p.partials = align_up(sizeof(float) * pf * 2 * (nt + 1));
     switch (kind) {
         case SAGA_GCN: p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0)); break;  // Y bf16
-        case SAGA_SAGE: p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0)); break;  // M bf16
+        case SAGA_SAGE:
+            p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0));                // M bf16 (two-kernel path)
+            p.inter1 = align_up(saga::sage_fused_workspace_bytes(std::max(o.out_dim, 0)));     // W^T image (fused)
+            break;
         case SAGA_GAT:
             p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0));               // z bf16
             p.inter1 = align_up(sizeof(float) * n * 8);                                         // el
@@ -383,6 +386,19 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (!(o.in_dim == 64 || o.in_dim == 128) || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
                 return fail(SAGA_EUNSUPPORTED, "SAGE supports in_dim in {64,128}, out_dim in {64,128,256}");
             if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE act must be NONE/RELU");
+            if (o.fused && !sage_fused_supported(o.in_dim, o.out_dim))
+                return fail(SAGA_EUNSUPPORTED, "fused SAGE supports in_dim 128, out_dim 64 or 128");
+            if (o.fused) {
+                // NEXT-1: mean aggregation and the concat-GEMM in one kernel
+                {
+                    ProfScope ps_("sage_fused_tc", st);
+                    e = launch_sage_fused(d, static_cast<const __nv_bfloat16 *>(x->data), o.in_dim,
+                                          static_cast<const __nv_bfloat16 *>(w->W), o.out_dim, w->bias, o.act,
+                                          static_cast<__nv_bfloat16 *>(out->data), i1, st, &why);
+                }
+                if (e) return fail(SAGA_ECUDA, "sage fused: %s (%s)", cudaGetErrorString(e), why);
+                return SAGA_OK;
+            }
             __nv_bfloat16 *M = reinterpret_cast<__nv_bfloat16 *>(i0);
             {
                 ProfScope ps_("agg_mean_bf16", st);

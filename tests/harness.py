@@ -34,8 +34,9 @@ def gpu_step(saga, cfg, g, d, layers=None, outs=None):
         return [lay(d["X"], {"W": d["W"], "bias": d["b"]}, out=o(0))], [lay]
     if cfg.model == "sage":
         f0, f1, f2 = cfg.dims
-        l1 = layers[0] if layers else saga.Layer("sage", g, f0, f1, act_relu, dt)
-        l2 = layers[1] if layers else saga.Layer("sage", g, f1, f2, saga.SAGA_ACT_NONE, dt)
+        fz = cfg.extra.get("fused", False)   # NEXT-1: Gather + concat-GEMM in one kernel
+        l1 = layers[0] if layers else saga.Layer("sage", g, f0, f1, act_relu, dt, fused=fz)
+        l2 = layers[1] if layers else saga.Layer("sage", g, f1, f2, saga.SAGA_ACT_NONE, dt, fused=fz)
         h1 = l1(d["X"], {"W": d["W1"]}, out=o(0))
         return [h1, l2(h1, {"W": d["W2"]}, out=o(1))], [l1, l2]
     if cfg.model == "gat":

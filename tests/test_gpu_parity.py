@@ -285,3 +285,35 @@ def test_ggnn_aggregators(saga, agg, relu):
                       act=1 if relu else 0, agg=agg)
     err = oracle.rel_err(y.cpu().numpy(), ref)
     assert err <= H.TOL["f32"], f"ggnn {agg} relu={relu}: rel err {err:.3e}"
+
+
+def _fused(cfg, n=None, m=None, name=None):
+    c = W.scaled(cfg, n or cfg.n, m or cfg.m, name or cfg.name + "f")
+    c.extra["fused"] = True
+    return c
+
+
+@pytest.mark.parametrize("size", ["full", "ragged", "tiny"])
+def test_sage_fused_next1(saga, size):
+    """NEXT-1: GraphSAGE-mean Gather fused with the tcgen05 concat-GEMM (one
+    kernel per layer) at C2 full size, a ragged size (last tile partial,
+    hubs split across warps) and a graph smaller than one tile."""
+    c = W.CONFIGS["C2"]
+    cfg = {"full": _fused(c), "ragged": _fused(c, 3001, 40000), "tiny": _fused(c, 77, 300)}[size]
+    _config_check(saga, cfg)
+
+
+@pytest.mark.parametrize("name,n,s,d", ZOO, ids=lambda x: x if isinstance(x, str) else "")
+def test_sage_fused_zoo(saga, name, n, s, d):
+    cfg = W.Config("zf", "sage", "er", n, s.shape[0], False, False, "bf16", (128, 128, 64), extra={"fused": True})
+    x = _zoo_inputs("sage", n, s, d, 7)
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, _ = H.gpu_step(saga, cfg, g, dx)
+    torch.cuda.synchronize()
+    og = H.oracle_graph(oracle, cfg, x)
+    refs = H.oracle_step(oracle, cfg, og, x, layer_inputs=[None, outs[0].cpu()])
+    for y, ref in zip(outs, refs):
+        err = oracle.rel_err(H.to_np(y), ref)
+        assert err <= H.TOL["bf16"], f"fused sage/{name}: rel err {err:.3e}"
