@@ -21,8 +21,8 @@
 // kernels give 2.0e-5 there.
 //
 // Kernel (persistent, one CTA per SM, 448 threads):
-//   warp 0      TMA producer: per 32-wide K block, the fp32 A tile (128 rows,
-//               128-byte swizzle; A may come from two tensors along K) and the
+//   warp 0      TMA producer: per 16-wide K block, the fp32 A tile (128 rows,
+//               64-byte swizzle; A may come from two tensors along K) and the
 //               pre-split B_hi / B_lo tiles (BN rows of W^T),
 //   warp 1      TMEM owner + single-thread tcgen05.mma.kind::tf32 issuer
 //               (M = 128, N = BN, K = 8): 3 MMAs per K step,
@@ -50,8 +50,13 @@ namespace {
 constexpr int kEpiWarps = 8;                // two per TMEM lane quarter, each half the columns
 constexpr int kThreads = 192 + 32 * kEpiWarps;
 constexpr int kBM = 128;
-constexpr int kBK = 32;                     // fp32 per 128-byte swizzle row
-constexpr int kATile = kBM * kBK * 4;       // 16 KB
+// K block: 16 fp32 = one 64-byte swizzle row, so a ring stage (A, A_lo,
+// B_hi, B_lo) is half the 128-byte-block size and twice as many K blocks are
+// in flight (the per-block producer -> converter -> MMA hand-offs, not the
+// bytes, bound the message GEMMs).
+constexpr int kBK = 16;
+constexpr int kATile = kBM * kBK * 4;       // 8 KB
+constexpr int kMaxStages = 8;
 constexpr int kSmemLimit = 232448;
 
 enum { EPI_MSG = 0, EPI_GRU = 1 };
@@ -60,13 +65,14 @@ template <int BN>
 struct Layout {
     static constexpr int kBTile = BN * kBK * 4;                 // one of B_hi / B_lo
     static constexpr int kStage = 2 * kATile + 2 * kBTile;     // A(hi in place), A_lo, B_hi, B_lo
-    static constexpr int kStages = (kSmemLimit - 2048) / kStage > 4 ? 4 : (kSmemLimit - 2048) / kStage;
+    static constexpr int kStages =
+        (kSmemLimit - 2048) / kStage > kMaxStages ? kMaxStages : (kSmemLimit - 2048) / kStage;
     static constexpr int kBytes = 1024 + kStages * kStage + 1024;
     static_assert(kStages >= 2, "need a double-buffered ring");
 };
 
 struct alignas(8) Bars {
-    uint64_t full[4], conv[4], empty[4], tfull[2], tempty[2];
+    uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
     uint32_t tmem_base;
 };
 
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // the m part runs N = 192 over [gin r z] and the h part N = 192
             // over [r z ghn] -- 25% fewer MMAs
             constexpr uint32_t idesc192 = ptx::make_idesc(2 /*TF32*/, kBM, 192);
-            constexpr uint32_t kRow64 = 64 * 128;  // 64 B^T rows (1024-B aligned swizzle atoms)
+            constexpr uint32_t kRow64 = 64 * kBK * 4;  // 64 B^T rows (whole 512-B swizzle atoms)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -184,18 +190,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (EPI == EPI_GRU && (kb | k) != 0) {
                             const bool hpart = kb >= KB0;
                             const uint32_t dd = d + (hpart ? 64 : 0), bo = hpart ? kRow64 : 0;
-                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(bhi + bo + off),
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw64(ahi + off), ptx::make_sdesc_sw64(bhi + bo + off),
                                            idesc192, 1);
-                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + bo + off),
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw64(ahi + off), ptx::make_sdesc_sw64(blo + bo + off),
                                            idesc192, 1);
-                            ptx::umma_tf32(dd, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(bhi + bo + off),
+                            ptx::umma_tf32(dd, ptx::make_sdesc_sw64(alo + off), ptx::make_sdesc_sw64(bhi + bo + off),
                                            idesc192, 1);
                             continue;
                         }
-                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(bhi + off), idesc,
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw64(ahi + off), ptx::make_sdesc_sw64(bhi + off), idesc,
                                        (kb | k) != 0);
-                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(ahi + off), ptx::make_sdesc_sw128(blo + off), idesc, 1);
-                        ptx::umma_tf32(d, ptx::make_sdesc_sw128(alo + off), ptx::make_sdesc_sw128(bhi + off), idesc, 1);
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw64(ahi + off), ptx::make_sdesc_sw64(blo + off), idesc, 1);
+                        ptx::umma_tf32(d, ptx::make_sdesc_sw64(alo + off), ptx::make_sdesc_sw64(bhi + off), idesc, 1);
                     }
                     ptx::umma_commit(&bar->empty[stage]);  // frees the stage when these MMAs retire
                     if (++stage == L::kStages) { stage = 0; phase ^= 1; }
@@ -410,16 +416,16 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// 2-D fp32 row-major [rows][cols] (row stride ld floats) with a {32, box_rows} box, 128B swizzle.
+// 2-D fp32 row-major [rows][cols] (row stride ld floats) with a {kBK, box_rows} box, 64B swizzle.
 bool make_map_f32(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -163,6 +163,17 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// Same, 64-byte swizzle (16 fp32 per row): 512 B between 8-row groups, layout 4.
+__device__ __forceinline__ uint64_t make_sdesc_sw64(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(512 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(4) << 61;
+    return d;
+}
+
 // TMEM -> registers: 32 lanes x 32 bits, 32 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
