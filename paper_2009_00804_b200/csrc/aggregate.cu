@@ -62,6 +62,10 @@ struct GraphView {
 GraphView view(const GraphDev &g) {
     return GraphView{g.row_ptr, g.col_src, g.task_v, g.task_p, g.task_items, g.ntasks, g.n, (int32_t)g.e};
 }
+// the same CSR with the 4x finer schedule (GAT)
+GraphView view_fine(const GraphDev &g) {
+    return GraphView{g.row_ptr, g.col_src, g.ftask_v, g.ftask_p, g.ftask_items, g.fntasks, g.n, (int32_t)g.e};
+}
 // rows (v, t) -> r = v * num_etypes + t (built when the graph has edge types)
 GraphView view_typed(const GraphDev &g) {
     return GraphView{g.trow_ptr, g.tcol_src, g.ttask_v, g.ttask_p, g.ttask_items, g.tntasks,
@@ -718,7 +722,7 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
     GatOp op{z, el, er, slope, out};
-    return run<8, 4>(view(g), op, ws, st);
+    return run<8, 4>(view_fine(g), op, ws, st);
 }
 
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,

@@ -29,10 +29,16 @@ struct GraphDev {
     // Merge-path load-balance schedule (S6): items = E edges + N row ends,
     // task k covers items [k*T, min((k+1)T, E+N)); its start coordinate is
     // (task_v[k], task_p[k]).  Arrays have ntasks+1 entries.
+    // ~1 task per resident warp (32 per SM): the sum/mean/typed gathers.
     int64_t task_items = 0;       // T
     int64_t ntasks = 0;
     int32_t *task_v = nullptr;
     int64_t *task_p = nullptr;
+    // A 4x finer schedule of the same CSR for the GAT edge softmax, whose
+    // per-item cost varies more (its tail balances better over 4 tasks/warp).
+    int64_t ftask_items = 0, fntasks = 0;
+    int32_t *ftask_v = nullptr;
+    int64_t *ftask_p = nullptr;
     // Typed view (built when edge types are given): an internal CSR whose
     // rows are (destination, type) pairs r = v * num_etypes + t, edges in
     // (dst, type, COO index) order; the typed gathers (gated, R-GCN) are plain

@@ -142,7 +142,7 @@ struct Plan {
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
     Plan p;
     // the typed gathers run over the typed view's own schedule
-    const size_t nt = (size_t)std::max(g.ntasks, g.tntasks);
+    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks});
     const size_t n = (size_t)g.n;
     size_t width = 0;
     switch (kind) {
@@ -334,7 +334,8 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i0 = ws + plan.counters + plan.partials;
     uint8_t *i1 = i0 + plan.inter0;
     uint8_t *i2 = i1 + plan.inter1;
-    cudaError_t e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max(d.ntasks, d.tntasks) + 1), st);
+    cudaError_t e =
+        cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1), st);
     if (e) return cuda_fail(e, "memset counters");
     const char *why = "";
 
