@@ -336,8 +336,13 @@ __global__ void k_inv(int64_t m, const int32_t *__restrict__ deg, float *inv) {
 static cudaError_t merge_path_schedule(int32_t n, int64_t e, const int64_t *row_ptr, int64_t *T_out,
                                        int64_t *ntasks_out, int32_t **task_v, int64_t **task_p, cudaStream_t st,
                                        int tasks_per_sm = 32) {
+    static const int sms = [] {
+        int dev = 0, c = kNumSMs;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        return c;
+    }();
     const int64_t items = e + (int64_t)n;
-    const int64_t target = (int64_t)kNumSMs * tasks_per_sm;
+    const int64_t target = (int64_t)sms * tasks_per_sm;
     const int64_t T = std::max<int64_t>(8, (items + target - 1) / target);
     const int64_t ntasks = items > 0 ? (items + T - 1) / T : 0;
     *T_out = T;
@@ -421,10 +426,12 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
         cudaFreeAsync(keys, st);
     }
 
-    // 6. merge-path schedules: ~1 task per resident warp (32 per SM on 148
-    // SMs) for the sum/mean/typed gathers -- measured 1.5-11% faster than 2
-    // or 4 per warp at C2, C4, C5, C6, C8 (fewer split-row tickets and task
-    // prologues) -- and 4 per warp for GAT (7% faster than 1 per warp at C3)
+    // 6. merge-path schedules: exactly one task per resident warp (the
+    // gathers run 4 blocks x 8 warps per SM: 32 tasks per SM, one full wave)
+    // for the sum/mean/typed gathers -- 1.5-11% faster than 2 per warp at C2,
+    // C4, C5, C6, C8 (fewer split-row tickets and task prologues); 24 or 40
+    // per SM (a partial wave) are 5-40% slower at C5 -- and 4 per warp for
+    // GAT, whose per-item cost varies (7% faster than 1 per warp at C3)
     SAGA_TRY(merge_path_schedule(n, e, g->row_ptr, &g->task_items, &g->ntasks, &g->task_v, &g->task_p, st, 32));
     SAGA_TRY(merge_path_schedule(n, e, g->row_ptr, &g->ftask_items, &g->fntasks, &g->ftask_v, &g->ftask_p, st, 128));
 
