@@ -655,6 +655,43 @@ cudaError_t run(const GraphView &g, const Op &op, AggWorkspace ws, cudaStream_t 
     return cudaGetLastError();
 }
 
+// Small-degree graphs (every in-degree <= kRowwiseMaxDeg): one warp per row,
+// no merge-path tasks and no split rows.  Used for C1's fused GCN layer,
+// where the merge-path engine's per-task prologue and split-row tickets
+// dominated a 12K-edge graph.
+constexpr int32_t kRowwiseMaxDeg = 64;
+
+template <int U, int kMinB, typename Op>
+__global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__restrict__ row_ptr,
+                                                         const int32_t *__restrict__ col_src, int32_t n, const Op op,
+                                                         const float *Wg, const int32_t w_elems) {
+    extern __shared__ float Ws[];
+    if (Wg) {
+        for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    for (int32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); r < n; r += gridDim.x * kWarpsPerBlock) {
+        const int32_t p0 = (int32_t)__ldg(row_ptr + r), p1 = (int32_t)__ldg(row_ptr + r + 1);
+        const float rs = op.row_value(r, 0);
+        typename Op::Acc acc;
+        op.zero(acc);
+        for (int32_t q0 = p0; q0 < p1; q0 += 32) {
+            const int32_t cnt = min(32, p1 - q0);
+            const int32_t cs = lane < cnt ? __ldg(col_src + q0 + lane) : 0;
+            for (int j = 0; j < cnt; j += U) {
+                typename Op::Val val[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) val[u] = op.load(__shfl_sync(kFull, cs, (j + u) & 31), lane);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (j + u < cnt) op.add(acc, val[u], rs);
+            }
+        }
+        do_finish(op, r, acc, rs, lane, Ws, 0);
+    }
+}
+
 template <int kAct>
 cudaError_t agg_sum_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, const float *scale,
                          const float *bias, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
@@ -679,6 +716,13 @@ template <int NPL>
 cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                     const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st) {
     GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
+    if (g.max_in_deg <= kRowwiseMaxDeg) {
+        if (g.n == 0) return cudaSuccess;
+        const unsigned blocks = (unsigned)((g.n + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL>>
+            <<<blocks, kBlock, sizeof(float) * f_in * f_out, st>>>(g.row_ptr, g.col_src, g.n, op, W, f_in * f_out);
+        return cudaGetLastError();
+    }
     return run<8, NPL == 4 ? 2 : 3>(view(g), op, ws, st, W, f_in * f_out);
 }
 

@@ -30,25 +30,35 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 
 // ------------------------------------------------------------ range check ----
-__global__ void k_range_check(int32_t n, int64_t e, const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                              const int32_t *__restrict__ etype, int32_t T, unsigned long long *first_bad) {
+// S0 range check fused with S2 degree counting: in-range edges count into the
+// degrees (integer atomics: order-independent result), out-of-range ones
+// report their lowest COO index.
+__global__ void k_range_degrees(int32_t n, int64_t e, const int32_t *__restrict__ src,
+                                const int32_t *__restrict__ dst, const int32_t *__restrict__ etype, int32_t T,
+                                unsigned long long *first_bad, int32_t *in_deg, int32_t *out_deg) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t s = src[i], d = dst[i];
+        const int32_t s = src[i], d = dst[i];
         bool bad = s < 0 || s >= n || d < 0 || d >= n;
         if (etype) {
-            int32_t t = etype[i];
+            const int32_t t = etype[i];
             bad |= t < 0 || t >= T;
         }
-        if (bad) atomicMin(first_bad, (unsigned long long)i);
+        if (bad) {
+            atomicMin(first_bad, (unsigned long long)i);
+        } else {
+            atomicAdd(in_deg + d, 1);
+            atomicAdd(out_deg + s, 1);
+        }
     }
 }
 
-__global__ void k_degrees(int64_t e, const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                          int32_t *in_deg, int32_t *out_deg) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
-        atomicAdd(in_deg + dst[i], 1);   // integer atomics: order-independent result
-        atomicAdd(out_deg + src[i], 1);
-    }
+// max in-degree (read back with the range-check result)
+__global__ void k_max_deg(int32_t n, const int32_t *__restrict__ in_deg, unsigned long long *out) {
+    int32_t m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, in_deg[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
 }
 
 // ------------------------------------------------------------------- scan ----
@@ -368,24 +378,6 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     g->stream = st;
     *first_bad = -1;
 
-    // 1. range check (the library's only host sync)
-    if (e > 0) {
-        unsigned long long *bad_d;
-        SAGA_TRY(cudaMallocAsync(&bad_d, sizeof(unsigned long long), st));
-        SAGA_TRY(cudaMemsetAsync(bad_d, 0xFF, sizeof(unsigned long long), st));
-        k_range_check<<<grid_for(e, 256), 256, 0, st>>>(n, e, src, dst, etype, num_etypes, bad_d);
-        SAGA_TRY(cudaGetLastError());
-        unsigned long long bad_h = 0;
-        SAGA_TRY(cudaMemcpyAsync(&bad_h, bad_d, sizeof bad_h, cudaMemcpyDeviceToHost, st));
-        SAGA_TRY(cudaStreamSynchronize(st));
-        cudaFreeAsync(bad_d, st);
-        if (bad_h != ~0ull) {
-            *first_bad = (int64_t)bad_h;
-            *why = "COO entry out of range";
-            return SAGA_ERANGE;
-        }
-    }
-
     const size_t nn = (size_t)std::max(n, 1), ne = (size_t)std::max<int64_t>(e, 1);
     SAGA_TRY(cudaMallocAsync(&g->row_ptr, sizeof(int64_t) * (nn + 1), st));
     SAGA_TRY(cudaMallocAsync(&g->col_src, sizeof(int32_t) * ne, st));
@@ -398,9 +390,31 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     SAGA_TRY(cudaMemsetAsync(g->in_deg, 0, sizeof(int32_t) * nn, st));
     SAGA_TRY(cudaMemsetAsync(g->out_deg, 0, sizeof(int32_t) * nn, st));
 
-    // 2. degrees, 3. row_ptr
-    if (e > 0) k_degrees<<<grid_for(e, 256), 256, 0, st>>>(e, src, dst, g->in_deg, g->out_deg);
-    SAGA_TRY(cudaGetLastError());
+    // 1+2. range check and degrees in one pass, max in-degree; read back
+    // together (the library's only host sync)
+    {
+        unsigned long long *rb_d;  // [first bad edge, max in-degree]
+        SAGA_TRY(cudaMallocAsync(&rb_d, 2 * sizeof(unsigned long long), st));
+        SAGA_TRY(cudaMemsetAsync(rb_d, 0xFF, sizeof(unsigned long long), st));
+        SAGA_TRY(cudaMemsetAsync(rb_d + 1, 0, sizeof(unsigned long long), st));
+        if (e > 0)
+            k_range_degrees<<<grid_for(e, 256), 256, 0, st>>>(n, e, src, dst, etype, num_etypes, rb_d, g->in_deg,
+                                                              g->out_deg);
+        if (n > 0) k_max_deg<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, rb_d + 1);
+        SAGA_TRY(cudaGetLastError());
+        unsigned long long rb_h[2] = {0, 0};
+        SAGA_TRY(cudaMemcpyAsync(rb_h, rb_d, sizeof rb_h, cudaMemcpyDeviceToHost, st));
+        SAGA_TRY(cudaStreamSynchronize(st));
+        cudaFreeAsync(rb_d, st);
+        if (rb_h[0] != ~0ull) {
+            *first_bad = (int64_t)rb_h[0];
+            *why = "COO entry out of range";
+            return SAGA_ERANGE;
+        }
+        g->max_in_deg = (int32_t)rb_h[1];
+    }
+
+    // 3. row_ptr
     SAGA_TRY(scan_exclusive<int32_t>(g->in_deg, n, g->row_ptr, st));
 
     // 4. stable LSD radix sort of (dst, COO index)

@@ -26,6 +26,7 @@ struct GraphDev {
     float *dinv = nullptr;        // [n]  in_deg^-1/2 (0 if 0)  -- S1, GCN
     float *inv_deg = nullptr;     // [n]  1/in_deg (0 if 0)     -- S1, SAGE
     int32_t *deg_order = nullptr; // [n]  vertices by in-degree, descending (LSTM work queue)
+    int32_t max_in_deg = 0;       // host copy (read back with the range check)
     // Merge-path load-balance schedule (S6): items = E edges + N row ends,
     // task k covers items [k*T, min((k+1)T, E+N)); its start coordinate is
     // (task_v[k], task_p[k]).  Arrays have ntasks+1 entries.
