@@ -666,13 +666,19 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
                                                          const int32_t *__restrict__ col_src, int32_t n, const Op op,
                                                          const float *Wg, const int32_t w_elems) {
     extern __shared__ float Ws[];
+    const int lane = threadIdx.x & 31;
+    int32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    // the first row's bounds are in flight while the block stages W
+    int32_t p0 = r < n ? (int32_t)__ldg(row_ptr + r) : 0, p1 = r < n ? (int32_t)__ldg(row_ptr + r + 1) : 0;
     if (Wg) {
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
         __syncthreads();
     }
-    const int lane = threadIdx.x & 31;
-    for (int32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); r < n; r += gridDim.x * kWarpsPerBlock) {
-        const int32_t p0 = (int32_t)__ldg(row_ptr + r), p1 = (int32_t)__ldg(row_ptr + r + 1);
+    for (; r < n; r += gridDim.x * kWarpsPerBlock) {
+        if (r != blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) {
+            p0 = (int32_t)__ldg(row_ptr + r);
+            p1 = (int32_t)__ldg(row_ptr + r + 1);
+        }
         const float rs = op.row_value(r, 0);
         typename Op::Acc acc;
         op.zero(acc);
@@ -716,7 +722,7 @@ template <int NPL>
 cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                     const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st) {
     GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
-    if (g.max_in_deg <= kRowwiseMaxDeg) {
+    if (gcn_f32_rowwise(g)) {
         if (g.n == 0) return cudaSuccess;
         const unsigned blocks = (unsigned)((g.n + kWarpsPerBlock - 1) / kWarpsPerBlock);
         k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL>>
@@ -789,5 +795,7 @@ cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t 
     if (relu) return run<4, 4>(view(g), EdgeMlpOp<false, true>{AB, m}, ws, st);
     return run<4, 4>(view(g), EdgeMlpOp<false, false>{AB, m}, ws, st);
 }
+
+bool gcn_f32_rowwise(const GraphDev &g) { return g.max_in_deg <= kRowwiseMaxDeg; }
 
 }  // namespace saga

@@ -71,6 +71,9 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads);
 cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
                                 __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
 // C1 / fp32 GCN fused: out[v] = act((dinv[v] * sum dinv[u] x[u]) . W + bias).
+// True when launch_gcn_f32_fused runs one warp per row (no split-row tickets,
+// so saga_layer skips zeroing the ticket counters).
+bool gcn_f32_rowwise(const GraphDev &g);
 cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                                  const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st);
 // SAGE: M[v] = inv_deg[v] * sum x[u]  (bf16 out)

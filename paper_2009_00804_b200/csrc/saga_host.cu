@@ -334,9 +334,12 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i0 = ws + plan.counters + plan.partials;
     uint8_t *i1 = i0 + plan.inter0;
     uint8_t *i2 = i1 + plan.inter1;
-    cudaError_t e =
-        cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1), st);
-    if (e) return cuda_fail(e, "memset counters");
+    cudaError_t e = cudaSuccess;
+    if (!(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {  // split-row tickets start at 0
+        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1),
+                            st);
+        if (e) return cuda_fail(e, "memset counters");
+    }
     const char *why = "";
 
     switch (kind) {
