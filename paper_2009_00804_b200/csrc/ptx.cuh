@@ -202,53 +202,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// --------------------------------------------------------- global loads ----
-// 16-byte read-only load with an L2 eviction-priority hint.
-__device__ __forceinline__ uint4 ldg_nc_v4_policy(const void *p, uint64_t policy) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p), "l"(policy));
-    return r;
-}
-// Feature-row gather load.  mode 0: L1 no-allocate (L2 treats it as
-// evict-first); 1: plain non-coherent (L2 evict-normal); 2: L1 no-allocate
-// with an explicit L2 cache-policy register.
-__device__ __forceinline__ uint4 ldg_row_v4(const void *p, int mode, uint64_t policy) {
-    uint4 r;
-    if (mode == 1)
-        asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    else if (mode == 2)
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                     : "l"(p), "l"(policy));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                     : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-// Bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2.
-__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Streaming 16-byte store (L2 evict-first cache policy).
-__device__ __forceinline__ void stg_v4_stream(void *p, uint4 v) {
-    asm volatile(
-        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-        "st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, pol;\n}" ::"l"(p),
-        "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-        : "memory");
-}
-
 // acc += w.lo * h.lo + w.hi * h.hi with bf16 x bf16 products in fp32
 // (sm_100 mixed-precision FMA: two FHFMA.BF16, no unpacking).
 __device__ __forceinline__ void fma_bf16x2_f32(float &acc, uint32_t w, uint32_t h) {
