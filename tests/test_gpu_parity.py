@@ -367,3 +367,26 @@ def test_random_graphs(saga, model, seed):
     for y, ref in zip(outs, refs):
         err = oracle.rel_err(H.to_np(y), ref)
         assert err <= tol, f"{model}/seed {seed} (n={n}, e={s.shape[0]}): rel err {err:.3e}"
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C8"])
+def test_cuda_graph_replay_matches_eager(saga, cfg):
+    """bench.py times the step captured in a CUDA graph: the replayed step is
+    bit-identical to the eagerly launched one (same kernels, deterministic)."""
+    c = W.CONFIGS[cfg]
+    if c.n > 200000:
+        c = W.scaled(c, 20000, 200000, cfg + "g")
+    d = W.make_inputs(c, DEV)
+    g = H.gpu_graph(saga, c, d)
+    outs, layers = H.gpu_step(saga, c, g, d)
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs]
+    for o in outs:
+        o.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        H.gpu_step(saga, c, g, d, layers, outs)
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
