@@ -546,6 +546,16 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         if (lane == 0) VW.wr = wbase;
         __syncwarp();
     };
+    // col_src in 32-edge chunks, two chunks ahead of the one in use (one
+    // chunk -- 4 batches -- left 10% of the C5 stalls on the col_src load);
+    // the first three are issued before the row window is filled, so the two
+    // prologue round trips overlap
+    auto load_cs = [&](int32_t base) -> int32_t {
+        const int32_t q = base + lane;
+        return q < p1 ? __ldcs(g.col_src + q) : 0;
+    };
+    int32_t cb = p;
+    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32), cs_c = load_cs(cb + 64);
     const int32_t v0 = v;
     const int32_t head_beg = (int32_t)g.row_ptr[v];
     bool head_open = head_beg < p;  // the first row began in an earlier task (its partial is pending)
@@ -580,14 +590,6 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         begin_row_of(op, acc, v, g.n, lane);
     };
 
-    auto load_cs = [&](int32_t base) -> int32_t {
-        const int32_t q = base + lane;
-        return q < p1 ? __ldcs(g.col_src + q) : 0;
-    };
-    // col_src in 32-edge chunks, two chunks ahead of the one in use (one
-    // chunk -- 4 batches -- left 10% of the C5 stalls on the col_src load)
-    int32_t cb = p;
-    int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32), cs_c = load_cs(cb + 64);
     // keeps q - cb < 32; batches start at p + multiple of U and U | 32, so a
     // batch never straddles a chunk
     auto slide = [&](int32_t q) {
