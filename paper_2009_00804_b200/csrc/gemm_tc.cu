@@ -38,7 +38,7 @@ constexpr int kCStageBytes = kBM * 64 * 2;    // 16 KB: 128 rows x 64 bf16 colum
 constexpr int kSmemLimit = 232448;            // 227 KB opt-in maximum
 
 struct alignas(8) Barriers {
-    uint64_t full[8], empty[8], tfull[2], tempty[2];
+    uint64_t full[8], empty[8], tfull[2], tempty[2], wready;
     uint32_t tmem_base;
     float vec[256];  // epilogue vectors staged once per CTA: bias[BN], or GAT a_src[64] | a_dst[64]
 };
@@ -90,27 +90,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (M + kBM - 1) / kBM;
 
-    // ---- prologue: W -> shared (K-major, 128B swizzle), barriers, TMEM ----
-    {
-        const int K = KB * kBK;
-        const int chunks = KB * BN * 8;  // 16-byte chunks: (kb, n, kc)
-        for (int c = threadIdx.x; c < chunks; c += kThreads) {
-            const int n = c % BN;
-            const int kc = (c / BN) % 8;
-            const int kb = c / (BN * 8);
-            const int k0 = kb * kBK + kc * 8;
-            uint32_t w[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                __nv_bfloat16 lo = W[(int64_t)(k0 + 2 * i) * BN + n];
-                __nv_bfloat16 hi = W[(int64_t)(k0 + 2 * i + 1) * BN + n];
-                w[i] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
-            }
-            uint8_t *dst = Bs + kb * L::kBBytesPerKB + n * 128 + ((kc ^ (n & 7)) << 4);
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        (void)K;
-    }
+    // ---- prologue: barriers, epilogue vectors, TMEM (W is staged by the
+    // epilogue warps after the barrier, overlapping the first A loads) ----
     if (threadIdx.x == 0) {
         for (int s = 0; s < L::kStages; ++s) {
             ptx::mbar_init(&bar->full[s], 1);
@@ -120,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bar->tfull[a], 1);
             ptx::mbar_init(&bar->tempty[a], 128);
         }
+        ptx::mbar_init(&bar->wready, 128);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmA0);
         ptx::prefetch_tmap(&tmA1);
@@ -134,7 +116,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     if (warp == 1) ptx::tmem_alloc<2 * BN>(&bar->tmem_base);
-    ptx::fence_proxy_async_smem();  // W written by generic stores, read by UMMA
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -165,6 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            ptx::mbar_wait(&bar->wready, 0);  // W staged by the epilogue warps
+            ptx::tc_fence_after();
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
                 const int acc = it & 1;
                 const uint32_t aphase = (it >> 1) & 1;
@@ -192,6 +175,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;            // TMEM lane quarter this warp may access
         const int r = q * 32 + lane;       // row within the tile
         const int et = threadIdx.x - 64;   // 0..127
+        {   // W -> shared (K-major, 128-byte swizzle) while the first A tiles load.
+            // One unit = an 8(k) x 8(n) block: eight independent 16-byte loads
+            // along n (coalesced across threads), a register transpose, eight
+            // 16-byte smem stores (one K-major chunk per n).
+            if ((reinterpret_cast<uintptr_t>(W) & 15) == 0) {
+                const int units = KB * 8 * (BN / 8);
+                for (int c = et; c < units; c += 128) {
+                    const int n0 = (c % (BN / 8)) * 8;
+                    const int kc = (c / (BN / 8)) % 8;
+                    const int kb = c / BN;
+                    const int k0 = kb * kBK + kc * 8;
+                    uint4 v[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        v[r] = __ldg(reinterpret_cast<const uint4 *>(W + (int64_t)(k0 + r) * BN + n0));
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
+                        uint32_t w[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t *a = reinterpret_cast<const uint32_t *>(&v[2 * i]);
+                            const uint32_t *b = reinterpret_cast<const uint32_t *>(&v[2 * i + 1]);
+                            w[i] = __byte_perm(a[j >> 1], b[j >> 1], sel);
+                        }
+                        const int n = n0 + j;
+                        uint8_t *dst = Bs + kb * L::kBBytesPerKB + n * 128 + ((kc ^ (n & 7)) << 4);
+                        *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+            } else {
+                const int chunks = KB * BN * 8;  // 16-byte chunks: (kb, n, kc)
+                for (int c = et; c < chunks; c += 128) {
+                    const int n = c % BN;
+                    const int kc = (c / BN) % 8;
+                    const int kb = c / (BN * 8);
+                    const int k0 = kb * kBK + kc * 8;
+                    uint32_t w[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        __nv_bfloat16 lo = W[(int64_t)(k0 + 2 * i) * BN + n];
+                        __nv_bfloat16 hi = W[(int64_t)(k0 + 2 * i + 1) * BN + n];
+                        w[i] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+                    }
+                    uint8_t *dst = Bs + kb * L::kBBytesPerKB + n * 128 + ((kc ^ (n & 7)) << 4);
+                    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            ptx::fence_proxy_async_smem();  // generic stores -> visible to UMMA
+            ptx::mbar_arrive(&bar->wready);
+        }
         int it = 0;
         uint32_t cstage = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
