@@ -517,10 +517,12 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     using DW = DenseWarp<U, typename Op::Val, kWinD>;
     __shared__ DW warps[kWarpsPerBlock];
     extern __shared__ float Ws[];  // epilogue operand staged per block: fused-GEMV weight, or bias
+    griddep_launch();
     if (Wg) {
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
         __syncthreads();
     }
+    griddep_wait();  // features / messages come from the call's previous kernel
     DW &W = warps[threadIdx.x >> 5];
     volatile DW &VW = W;
     const int lane = threadIdx.x & 31;
@@ -653,8 +655,7 @@ cudaError_t run(const GraphView &g, const Op &op, AggWorkspace ws, cudaStream_t 
     if (g.ntasks == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((g.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const size_t smem = Wg ? sizeof(float) * w_elems : 0;
-    k_segreduce<U, kMinB, Op><<<blocks, kBlock, smem, st>>>(g, op, ws, Wg, w_elems);
-    return cudaGetLastError();
+    return launch(k_segreduce<U, kMinB, Op>, blocks, kBlock, smem, st, g, op, ws, Wg, w_elems);
 }
 
 // Small-degree graphs (every in-degree <= kRowwiseMaxDeg): one warp per row,
@@ -672,10 +673,12 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
     int32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     // the first row's bounds are in flight while the block stages W
     int32_t p0 = r < n ? (int32_t)__ldg(row_ptr + r) : 0, p1 = r < n ? (int32_t)__ldg(row_ptr + r + 1) : 0;
+    griddep_launch();
     if (Wg) {
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
         __syncthreads();
     }
+    griddep_wait();
     for (; r < n; r += gridDim.x * kWarpsPerBlock) {
         if (r != blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) {
             p0 = (int32_t)__ldg(row_ptr + r);
@@ -727,9 +730,8 @@ cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float
     if (gcn_f32_rowwise(g)) {
         if (g.n == 0) return cudaSuccess;
         const unsigned blocks = (unsigned)((g.n + kWarpsPerBlock - 1) / kWarpsPerBlock);
-        k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL>>
-            <<<blocks, kBlock, sizeof(float) * f_in * f_out, st>>>(g.row_ptr, g.col_src, g.n, op, W, f_in * f_out);
-        return cudaGetLastError();
+        return launch(k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL>>, blocks, kBlock,
+                      sizeof(float) * f_in * f_out, st, g.row_ptr, g.col_src, g.n, op, W, f_in * f_out);
     }
     return run<8, NPL == 4 ? 2 : 3>(view(g), op, ws, st, W, f_in * f_out);
 }

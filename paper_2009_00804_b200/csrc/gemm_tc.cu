@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== TMA producer =====================
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_first();  // A is streamed once
+            griddep_wait();  // A may come from the call's previous kernel
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::fence_proxy_async_smem();  // generic stores -> visible to UMMA
             ptx::mbar_arrive(&bar->wready);
         }
+        griddep_wait();  // before this grid's first global write
         int it = 0;
         uint32_t cstage = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -342,8 +344,7 @@ cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMa
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-    k_gemm_bf16_tc<BN><<<grid, kThreads, L::kBytes, st>>>(m0, m1, mc, a.W, a.M, KB, KB0, ep);
-    return cudaGetLastError();
+    return launch(k_gemm_bf16_tc<BN>, grid, kThreads, L::kBytes, st, m0, m1, mc, a.W, a.M, KB, KB0, ep);
 }
 
 }  // namespace

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             const uint64_t pol_a = ptx::policy_evict_first();  // A streamed once
             const uint64_t pol_b = ptx::policy_evict_last();   // B re-read by every CTA
+            griddep_wait();  // A and the split B come from the call's earlier kernels
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = (warp - 6) >> 2;
         const int r = q * 32 + lane;  // row within the tile
         int it = 0;
+        griddep_wait();  // before this grid's first global write
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
@@ -334,6 +336,7 @@ __device__ __forceinline__ float gru_bt(int f, const float *__restrict__ W_ih, c
 __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_ih,
                                 const float *__restrict__ W_hh, float *bm_hi, float *bm_lo, float *bg_hi,
                                 float *bg_lo) {
+    griddep_wait();
     const int nm = f * T * f, ng = 4 * f * 2 * f;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nm + ng; i += gridDim.x * blockDim.x) {
         float x;
@@ -359,6 +362,7 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
 __global__ void k_split_ggnn(int f, const float *__restrict__ W_e, const float *__restrict__ b_e,
                              const float *__restrict__ W_ih, const float *__restrict__ W_hh, float *be_hi,
                              float *be_lo, float *bias2, float *bg_hi, float *bg_lo) {
+    griddep_wait();
     const int ne = 2 * f * f, ng = 4 * f * 2 * f;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ne + ng + 2 * f; i += gridDim.x * blockDim.x) {
         if (i >= ne + ng) {
@@ -388,6 +392,7 @@ __global__ void k_split_ggnn(int f, const float *__restrict__ W_e, const float *
 // k >= T f from W_self[k - T f][n]  (N = f_out = f, K = (T + 1) f).
 __global__ void k_split_rgcn(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_self,
                              float *b_hi, float *b_lo) {
+    griddep_wait();
     const int K = (T + 1) * f, total = f * K;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int n = i / K, k = i % K;
@@ -443,9 +448,8 @@ cudaError_t launch_tf32split(const CUtensorMap &a0, const CUtensorMap &a1, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (M + kBM - 1) / kBM * n_tiles;
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-    k_gemm_tf32split<BN, EPI><<<grid, kThreads, L::kBytes, st>>>(a0, a1, bhi, blo, M, KB, KB0, n_tiles, msg_out, ld_out,
-                                                                gru);
-    return cudaGetLastError();
+    return launch<false>(k_gemm_tf32split<BN, EPI>, grid, kThreads, L::kBytes, st, a0, a1, bhi, blo, M, KB, KB0, n_tiles,
+                  msg_out, ld_out, gru);
 }
 
 }  // namespace
@@ -462,8 +466,7 @@ cudaError_t launch_rgcn_apply_tc(int64_t M, int32_t f, int32_t T, const float *S
     }
     const int K = (T + 1) * f;
     float *b_hi = wsplit, *b_lo = wsplit + (size_t)f * K;
-    k_split_rgcn<<<256, 256, 0, st>>>(f, T, W_type, W_self, b_hi, b_lo);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch<false>(k_split_rgcn, 256, 256, 0, st, f, T, W_type, W_self, b_hi, b_lo);
     if (e) return e;
     CUtensorMap aS, aH, bh, bl;
     if (!make_map_f32(&aS, S, M, (int64_t)T * f, (int64_t)T * f, kBM) || !make_map_f32(&aH, H, M, f, f, kBM) ||
@@ -488,8 +491,7 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
     }
     float *bm_hi = wsplit, *bm_lo = bm_hi + (size_t)f * T * f;
     float *bg_hi = bm_lo + (size_t)f * T * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
-    k_split_weights<<<256, 256, 0, st>>>(f, T, W_type, W_ih, W_hh, bm_hi, bm_lo, bg_hi, bg_lo);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch<false>(k_split_weights, 256, 256, 0, st, f, T, W_type, W_ih, W_hh, bm_hi, bm_lo, bg_hi, bg_lo);
     if (e) return e;
     CUtensorMap aS, aM, aH, bmh, bml, bgh, bgl;
     if (!make_map_f32(&aS, S, M, (int64_t)T * f, (int64_t)T * f, kBM) || !make_map_f32(&aM, m_ws, M, f, f, kBM) ||
@@ -518,8 +520,7 @@ cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const floa
     }
     float *be_hi = wsplit, *be_lo = be_hi + (size_t)2 * f * f, *bias2 = be_lo + (size_t)2 * f * f;
     float *bg_hi = bias2 + 2 * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
-    k_split_ggnn<<<256, 256, 0, st>>>(f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch<false>(k_split_ggnn, 256, 256, 0, st, f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
     if (e) return e;
     CUtensorMap aH, bh, bl;
     if (!make_map_f32(&aH, H, M, f, f, kBM) || !make_map_f32(&bh, be_hi, 2 * f, f, f, 128) ||

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <utility>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -11,6 +12,45 @@
 namespace saga {
 
 constexpr int kNumSMs = 148;
+
+// ---- Programmatic dependent launch (PDL) ----------------------------------
+// Inside one saga_layer call every kernel after the first is launched with
+// programmatic stream serialisation: it may be scheduled while its
+// predecessor drains (its launch latency and prologue -- barrier init, TMEM
+// allocation, weight staging -- overlap the predecessor's tail).  Contract
+// for every kernel launched through saga::launch: (1) it calls griddep_wait()
+// before touching memory an earlier kernel of the call writes (and before any
+// global write), so the grid cannot complete before its predecessor (the
+// chain stays transitive); (2) it may call griddep_launch() to let its own
+// dependent be scheduled early.  Both are no-ops for a normal launch.  The
+// first kernel of a call is a normal launch, so it is ordered after all
+// earlier work of the stream (the caller's writes to x and the weights).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Host side: g_pdl_call is set by saga_layer for the duration of a call
+// (never while per-kernel profiling records events between the kernels);
+// g_pdl_armed becomes true after the call's first launch.
+extern thread_local bool g_pdl_call, g_pdl_armed;
+
+// kPdl = false: always a normal launch (kernels measured slower as PDL
+// secondaries: the split-TF32 GEMMs and their weight-split kernels).
+template <bool kPdl = true, typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = kPdl && g_pdl_armed ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    if (g_pdl_call) g_pdl_armed = true;
+    return e;
+}
 
 // Device arrays owned by a built graph (saga_graph_build, S0).
 struct GraphDev {

@@ -54,8 +54,11 @@ struct LstmSmem {
 __device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 // wt[j][g][c] = W_hh[g][8c .. 8c+7][j] (bf16): row (unit j, gate g) of W_hh^T, 256 contiguous bytes
-__global__ void k_stage_whh(const __nv_bfloat16 *__restrict__ W_hh, uint4 *wt) {
+// (thread 0 also resets the gather's work-queue head)
+__global__ void k_stage_whh(const __nv_bfloat16 *__restrict__ W_hh, uint4 *wt, int32_t *queue) {
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over kF * 4 * kF / 8 chunks
+    if (i == 0) *queue = 0;
     if (i >= 4 * kF * kF / 8) return;
     const int c = i % (kF / 8), g = (i / (kF / 8)) % 4, j = i / (kF / 8 * 4);
     uint32_t q[4];
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const float *__restrict__ b_ih, const float *__restrict__ b_hh,          // [4][kF]
                   __nv_bfloat16 *__restrict__ h_out, int32_t *queue) {
     __shared__ LstmSmem S;
+    griddep_wait();  // P, W_hh^T and the queue head come from the call's earlier kernels
     // thread -> (unit j, gate g): the 4 gates of a unit are adjacent lanes,
     // so the cell update gathers them with shuffles and a step needs ONE
     // barrier (the h broadcast)
@@ -138,8 +142,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-__global__ void k_zero_i32(int32_t *p) { *p = 0; }
-
 }  // namespace
 
 size_t lstm_workspace_bytes() { return sizeof(uint4) * 4 * kF * kF / 8; }
@@ -149,15 +151,14 @@ cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const 
                                void *wt_ws, cudaStream_t st) {
     if (g.n == 0) return cudaSuccess;
     uint4 *wt = static_cast<uint4 *>(wt_ws);
-    k_stage_whh<<<(4 * kF * kF / 8 + 255) / 256, 256, 0, st>>>(W_hh, wt);
-    k_zero_i32<<<1, 1, 0, st>>>(queue);
+    cudaError_t e = launch(k_stage_whh, (4 * kF * kF / 8 + 255) / 256, 256, 0, st, W_hh, wt, queue);
+    if (e) return e;
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)(g.n < sms ? g.n : sms);
-    k_lstm_gather<<<grid, kThreads, 0, st>>>(g.n, g.row_ptr, g.col_src, g.deg_order, P, wt, b_ih, b_hh,
-                                                             h_out, queue);
-    return cudaGetLastError();
+    return launch(k_lstm_gather, grid, kThreads, 0, st, g.n, g.row_ptr, g.col_src, g.deg_order, P, wt, b_ih, b_hh,
+                  h_out, queue);
 }
 
 }  // namespace saga

@@ -20,6 +20,10 @@ struct saga_graph {
     saga::GraphDev d;
 };
 
+namespace saga {
+thread_local bool g_pdl_call = false, g_pdl_armed = false;
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -113,6 +117,25 @@ struct ProfScope {
         std::lock_guard<std::mutex> lk(g_prof.mu);
         g_prof.pending.push_back(r);
     }
+};
+
+// Scope of one saga_layer call for programmatic dependent launch
+// (internal.cuh); SAGA_NO_PDL=1 in the environment turns it off.
+struct PdlCall {
+    PdlCall() {
+        static const bool off = [] {
+            const char *v = getenv("SAGA_NO_PDL");
+            return v && *v && *v != '0';
+        }();
+        bool prof;
+        {
+            std::lock_guard<std::mutex> lk(g_prof.mu);
+            prof = g_prof.on;
+        }
+        saga::g_pdl_call = !off && !prof;
+        saga::g_pdl_armed = false;
+    }
+    ~PdlCall() { saga::g_pdl_call = saga::g_pdl_armed = false; }
 };
 
 // The graph arrays and the build's scratch come from the device's default
@@ -335,6 +358,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i1 = i0 + plan.inter0;
     uint8_t *i2 = i1 + plan.inter1;
     cudaError_t e = cudaSuccess;
+    PdlCall pdl_call;
     if (!(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {  // split-row tickets start at 0
         e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1),
                             st);

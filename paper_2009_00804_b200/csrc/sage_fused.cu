@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using S = Smem<FO>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    griddep_wait();  // the W^T image comes from k_stage_wt
     uint8_t *A = sm + S::kA;
     uint8_t *B = sm + S::kB;
     float4 *part = reinterpret_cast<float4 *>(sm + S::kPart);
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ((u ^ (n % 8)) << 4) (128-byte swizzle, K-major).
 template <int FO>
 __global__ void k_stage_wt(const __nv_bfloat16 *__restrict__ W, uint8_t *img) {
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over 4 * FO * 8 units
     if (i >= 4 * FO * 8) return;
     const int u = i % 8, nn = (i / 8) % FO, c = i / (8 * FO);
@@ -325,8 +327,7 @@ __global__ void k_stage_wt(const __nv_bfloat16 *__restrict__ W, uint8_t *img) {
 template <int FO>
 cudaError_t launch_fo(const GraphDev &g, const __nv_bfloat16 *X, const __nv_bfloat16 *W, const float *bias, int act,
                       __nv_bfloat16 *out, void *img, cudaStream_t st, const char **why) {
-    k_stage_wt<FO><<<(4 * FO * 8 + 255) / 256, 256, 0, st>>>(W, static_cast<uint8_t *>(img));
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch(k_stage_wt<FO>, (4 * FO * 8 + 255) / 256, 256, 0, st, W, static_cast<uint8_t *>(img));
     if (e) return e;
     CUtensorMap tmX;
     if (!make_map_bf16(&tmX, X, g.n, kF)) {
@@ -341,9 +342,8 @@ cudaError_t launch_fo(const GraphDev &g, const __nv_bfloat16 *X, const __nv_bflo
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int ntiles = (g.n + kRows - 1) / kRows;
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-    k_sage_fused<FO><<<grid, kThreads, S::kBytes, st>>>(tmX, g.n, g.row_ptr, g.col_src, g.inv_deg, X,
-                                                         static_cast<const uint8_t *>(img), bias, act, out);
-    return cudaGetLastError();
+    return launch(k_sage_fused<FO>, grid, kThreads, S::kBytes, st, tmX, g.n, g.row_ptr, g.col_src, g.inv_deg, X,
+                  static_cast<const uint8_t *>(img), bias, act, out);
 }
 
 }  // namespace
