@@ -177,8 +177,10 @@ def algorithmic(cfg):
         # AB = H . [W_a | W_b] + [0 | b_e]: H read, AB written (K = f, N = 2f)
         out["ggnn_edge_tf32x3"] = {"bytes": n * f * 4 + n * 2 * f * 4, "flops": 2 * n * f * 2 * f,
                                    "peak": "tensor_tf32x3"}
-        # per edge an A row (512 B); per row its B half and the m row written
-        out["agg_edge_mlp_f32"] = {"bytes": e * 4 + (n + 1) * 8 + e * f * 4 + n * f * 4 + n * f * 4,
+        # compulsory: col_src, row_ptr, AB read once (A and B halves), m written
+        # (the per-edge A-row gathers, 512 B each, are L2 traffic, as for the
+        # other gathers)
+        out["agg_edge_mlp_f32"] = {"bytes": e * 4 + (n + 1) * 8 + n * 2 * f * 4 + n * f * 4,
                                    "flops": 3 * e * f, "peak": "hbm"}
         # GRU over [m || h]: m, h read (h twice), h' written
         out["ggnn_gru_tf32x3"] = {"bytes": n * f * 4 * 4, "flops": 2 * n * 6 * f * f, "peak": "tensor_tf32x3"}

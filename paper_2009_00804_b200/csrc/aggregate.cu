@@ -477,13 +477,16 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
                                           int64_t re, const float *Ws) {
     const int lane = threadIdx.x & 31;
     const int64_t k1 = (rb + r) / T, k2 = (re + r) / T;
-    __threadfence();
+    // release the partial stores before the ticket; acquire the others'
+    // after winning (acq_rel, not the sequentially consistent __threadfence:
+    // MEMBAR.SC.GPU stalled the task tails, 10% of C2's warp samples)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     __syncwarp();
     int old = 0;
     if (lane == 0) old = atomicAdd(ws.counters + k2, 1);
     old = __shfl_sync(kFull, old, 0);
     if (old == (int)(k2 - k1)) {
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         typename Op::Acc m;
         op.zero(m);
         op.merge(m, ws.partials + (2 * k1 + 1) * Op::kSlot, lane);
