@@ -390,3 +390,34 @@ def test_cuda_graph_replay_matches_eager(saga, cfg):
     torch.cuda.synchronize()
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6", "C7", "C8"])
+def test_programmatic_launch_matches_serialised(saga, cfg):
+    """Inside a layer call every kernel after the first is a programmatic
+    dependent launch (internal.cuh); with per-kernel profiling on, the library
+    launches them fully serialised.  Both give bit-identical outputs (each
+    kernel waits for its predecessor before reading its output)."""
+    c = W.CONFIGS[cfg]
+    if c.n > 200000:
+        c = W.scaled(c, 30000, 400000, cfg + "p")
+    d = W.make_inputs(c, DEV)
+    g = H.gpu_graph(saga, c, d)
+    outs, layers = H.gpu_step(saga, c, g, d)          # programmatic
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs]
+    for o in outs:
+        o.zero_()
+    saga.saga_profile_enable(True)                    # serialised (event pairs between kernels)
+    try:
+        H.gpu_step(saga, c, g, d, layers, outs)
+        torch.cuda.synchronize()
+    finally:
+        saga.saga_profile_enable(False)
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
+    for _ in range(3):                                # back-to-back programmatic steps
+        H.gpu_step(saga, c, g, d, layers, outs)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
