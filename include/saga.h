@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SAGA_ABI_VERSION 3  /* 2: SAGA_GGNN, saga_layer_opts.aggregator; 3: .fused */
+#define SAGA_ABI_VERSION 4  /* 2: SAGA_GGNN, saga_layer_opts.aggregator; 3: .fused; 4: .workspace_zeroed */
 
 #if defined(__GNUC__)
 #define SAGA_API __attribute__((visibility("default")))
@@ -92,6 +92,12 @@ typedef struct {
     int32_t fused;            /* SAGE only: 1 = Gather and the concat-GEMM as ONE kernel    */
                               /* (in_dim 128, out_dim 64 or 128), 0 =   */
                               /* the two-kernel path (default; measured faster at C2)       */
+    int32_t workspace_zeroed; /* 1 = the caller guarantees the workspace's ticket-counter   */
+                              /* region is zero: the memory was zero-filled before its     */
+                              /* first saga_layer call, and since then only completed      */
+                              /* saga_layer calls (which leave it zero) have used it; the  */
+                              /* call then skips zeroing it (one memset node per call).    */
+                              /* 0 = the library zeroes it (contents ignored on entry)     */
 } saga_layer_opts;
 
 /* Weights (device, row-major, [in][out] orientation = x . W, reading A8).
@@ -196,8 +202,10 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *        F32, in_dim = out_dim = 128; edge types are ignored.
  *  features  [N][in_dim];  out  [N][out_dim] with the features' dtype
  *  workspace device scratch of at least saga_layer_workspace_bytes() bytes;
- *            contents on entry are ignored; it must not be shared by calls in
- *            flight on other streams.
+ *            contents on entry are ignored unless opts->workspace_zeroed = 1
+ *            (then its first bytes -- the split-row ticket counters -- must be
+ *            zero, which every completed call leaves them); it must not be
+ *            shared by calls in flight on other streams.
  * Never allocates, never synchronises.  Deterministic: identical inputs give
  * bit-identical outputs (no floating-point atomics).
  */

@@ -50,7 +50,7 @@ class saga_tensor(ctypes.Structure):
 class saga_layer_opts(ctypes.Structure):
     _fields_ = [("in_dim", ctypes.c_int32), ("out_dim", ctypes.c_int32), ("heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("act", ctypes.c_int32), ("leaky_slope", ctypes.c_float),
-                ("aggregator", ctypes.c_int32), ("fused", ctypes.c_int32)]
+                ("aggregator", ctypes.c_int32), ("fused", ctypes.c_int32), ("workspace_zeroed", ctypes.c_int32)]
 
 
 class saga_weights(ctypes.Structure):
@@ -208,9 +208,9 @@ def saga_free(g: Graph):
 
 
 def make_opts(in_dim, out_dim, act, heads=0, head_dim=0, leaky_slope=0.2, aggregator=0,
-              fused=0) -> saga_layer_opts:
+              fused=0, workspace_zeroed=0) -> saga_layer_opts:
     return saga_layer_opts(int(in_dim), int(out_dim), int(heads), int(head_dim), int(act), float(leaky_slope),
-                           int(aggregator), int(fused))
+                           int(aggregator), int(fused), int(workspace_zeroed))
 
 
 def saga_layer_workspace_bytes(kind, g: Graph, opts: saga_layer_opts) -> int:
@@ -243,11 +243,19 @@ class Layer:
         self.opts = make_opts(in_dim, out_dim, act, heads, head_dim, leaky_slope,
                               {"sum": 0, "max": 1}.get(aggregator, aggregator), int(fused))
         nbytes = saga_layer_workspace_bytes(self.kind, g, self.opts)
-        self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+        # zero-filled once and owned by this Layer: every completed call leaves
+        # its ticket counters zero, so calls skip re-zeroing them
+        self.workspace = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+        self._filled = torch.cuda.Event()          # the first call's stream waits for the fill
+        self._filled.record()
+        self.opts.workspace_zeroed = 1
         self.out_shape = (g.num_vertices, out_dim)
         self.dtype = dtype
 
     def __call__(self, features, weights: dict, out=None, stream=None):
         if out is None:
             out = torch.empty(self.out_shape, dtype=self.dtype, device=features.device)
+        if self._filled is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self._filled)
+            self._filled = None
         return saga_layer(self.kind, self.g, features, weights, out, self.opts, self.workspace, stream)

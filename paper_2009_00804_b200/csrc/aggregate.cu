@@ -490,6 +490,7 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
     old = __shfl_sync(kFull, old, 0);
     if (old == (int)(k2 - k1)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (lane == 0) ws.counters[k2] = 0;  // every contributor has taken its ticket: leave it zero
         typename Op::Acc m;
         op.zero(m);
         op.merge(m, ws.partials + (2 * k1 + 1) * Op::kSlot, lane);

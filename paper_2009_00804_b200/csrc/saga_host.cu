@@ -359,7 +359,9 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i2 = i1 + plan.inter1;
     cudaError_t e = cudaSuccess;
     PdlCall pdl_call;
-    if (!(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {  // split-row tickets start at 0
+    // split-row tickets start at 0; every ticket's winner resets its counter,
+    // so a completed call leaves them zero (opts.workspace_zeroed skips this)
+    if (!o.workspace_zeroed && !(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {
         e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1),
                             st);
         if (e) return cuda_fail(e, "memset counters");
@@ -534,8 +536,9 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (e) return fail(SAGA_ECUDA, "lstm input gemm: %s (%s)", cudaGetErrorString(e), why);
             {
                 ProfScope ps_("lstm_gather", st);
+                // the work-queue head lives in the counters' spare last slot (never a ticket)
                 e = launch_lstm_gather(d, P, static_cast<const __nv_bfloat16 *>(w->W_hh), w->b_ih, w->b_hh, hagg,
-                                       aw.counters, i2, st);
+                                       aw.counters + std::max({d.ntasks, d.tntasks, d.fntasks}), i2, st);
             }
             if (e) return cuda_fail(e, "lstm gather");
             GemmArgs a;

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_error_string(lib):
-    assert lib.saga_abi_version() == 3
+    assert lib.saga_abi_version() == 4
     assert isinstance(lib.saga_last_error(), str)
 
 

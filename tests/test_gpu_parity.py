@@ -421,3 +421,33 @@ def test_programmatic_launch_matches_serialised(saga, cfg):
     torch.cuda.synchronize()
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6", "C7", "C8"])
+def test_workspace_zeroed_contract(saga, cfg):
+    """opts.workspace_zeroed (include/saga.h): with 0 the library zeroes the
+    ticket counters itself (a garbage-filled workspace gives the same output);
+    every completed call leaves them zero, so the next call may pass 1."""
+    c = W.CONFIGS[cfg]
+    if c.n > 200000:
+        c = W.scaled(c, 30000, 400000, cfg + "w")
+    d = W.make_inputs(c, DEV)
+    g = H.gpu_graph(saga, c, d)
+    outs, layers = H.gpu_step(saga, c, g, d)          # Layer: zero-filled workspace, flag 1
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs]
+    for lay in layers:
+        lay.workspace.fill_(0xAB)
+        lay.opts.workspace_zeroed = 0
+    H.gpu_step(saga, c, g, d, layers, outs)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
+    for lay in layers:
+        lay.opts.workspace_zeroed = 1                 # left zero by the call above
+    for o in outs:
+        o.zero_()
+    H.gpu_step(saga, c, g, d, layers, outs)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
