@@ -97,6 +97,41 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanhf_(float x) { return 2.0f * sigmoidf_(2.0f * x) - 1.0f; }
 
+// Rows row0 + lane (lane 0..31) of a [M][ld] fp32 matrix, columns col0 .. col0+31,
+// one row per lane in x[32].  Three butterfly stages (shfl_xor 1, 2, 4) transpose
+// each 8-lane group's 8 x 8 block of float4: afterwards lane j of group g holds
+// float4 j of rows 8g .. 8g+7, and store k writes row 8g + k's 128 bytes with
+// the group's 8 lanes.  Rows >= M are skipped.
+__device__ __forceinline__ void store_rows_coalesced(float (&x)[32], float *out, int ld, int64_t row0, int col0,
+                                                     int64_t M, int lane) {
+    const int j = lane & 7, g = lane >> 3;
+#pragma unroll
+    for (int s = 1; s < 8; s <<= 1) {
+        const bool hi = (j & s) != 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k & s) continue;
+            // the slot of the pair (k, k|s) whose bit s differs from the lane's
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float send = hi ? x[4 * k + e] : x[4 * (k | s) + e];
+                const float recv = __shfl_xor_sync(0xffffffffu, send, s);
+                if (hi)
+                    x[4 * k + e] = recv;
+                else
+                    x[4 * (k | s) + e] = recv;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int64_t row = row0 + 8 * g + k;
+        if (row < M)
+            reinterpret_cast<float4 *>(out + row * ld + col0)[j] =
+                make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+    }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tf32split(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
@@ -256,18 +291,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t v[32];
                     ptx::tmem_ld32(tbase + c * 32, v);
                     ptx::tmem_ld_wait();
-                    if (row < M) {
-                        const int col0 = nt * BN + c * 32;
-                        float x[32];
+                    const int col0 = nt * BN + c * 32;
+                    float x[32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            x[j] = __uint_as_float(v[j]) + (gru.bias ? __ldg(gru.bias + col0 + j) : 0.0f);
-                            if (gru.relu) x[j] = fmaxf(x[j], 0.0f);
-                        }
-                        float4 *o = reinterpret_cast<float4 *>(msg_out + row * ld_out + col0);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+                    for (int j = 0; j < 32; ++j) {
+                        x[j] = __uint_as_float(v[j]) + (gru.bias ? __ldg(gru.bias + col0 + j) : 0.0f);
+                        if (gru.relu) x[j] = fmaxf(x[j], 0.0f);
                     }
+                    // lane = row holds 32 contiguous columns: transpose 8x8 blocks of
+                    // float4 within each 8-lane group so that every store instruction
+                    // writes 4 whole 128-byte row segments (one per group) instead of
+                    // 32 scattered 16-byte pieces
+                    store_rows_coalesced(x, msg_out, ld_out, (t / n_tiles) * kBM + q * 32, col0, M, lane);
                 }
             } else {
                 // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt); this warp: 32 units, 16 at a time
