@@ -97,19 +97,22 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanhf_(float x) { return 2.0f * sigmoidf_(2.0f * x) - 1.0f; }
 
-// Rows row0 + lane (lane 0..31) of a [M][ld] fp32 matrix, columns col0 .. col0+31,
-// one row per lane in x[32].  Three butterfly stages (shfl_xor 1, 2, 4) transpose
-// each 8-lane group's 8 x 8 block of float4: afterwards lane j of group g holds
-// float4 j of rows 8g .. 8g+7, and store k writes row 8g + k's 128 bytes with
-// the group's 8 lanes.  Rows >= M are skipped.
-__device__ __forceinline__ void store_rows_coalesced(float (&x)[32], float *out, int ld, int64_t row0, int col0,
-                                                     int64_t M, int lane) {
-    const int j = lane & 7, g = lane >> 3;
+// Row-per-lane tiles <-> coalesced row segments.  A warp holds rows row0 + lane
+// (lane 0..31) of a [M][ld] fp32 matrix, G float4 (columns col0 .. col0+4G-1)
+// per lane in x[4G].  transpose_groups<G> transposes each G-lane group's G x G
+// block of float4 with log2(G) butterfly stages (shfl_xor 1, 2, 4): afterwards
+// lane j of group g holds float4 j of rows G g .. G g + G-1 (slot k = row G g + k);
+// it is its own inverse.  The store / load below then move whole 16G-byte row
+// segments per instruction (32/G rows each) instead of 32 scattered 16-byte
+// pieces.  Rows >= M are skipped (loads give 0).
+template <int G>
+__device__ __forceinline__ void transpose_groups(float (&x)[4 * G], int lane) {
+    const int j = lane & (G - 1);
 #pragma unroll
-    for (int s = 1; s < 8; s <<= 1) {
+    for (int s = 1; s < G; s <<= 1) {
         const bool hi = (j & s) != 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < G; ++k) {
             if (k & s) continue;
             // the slot of the pair (k, k|s) whose bit s differs from the lane's
 #pragma unroll
@@ -123,13 +126,34 @@ __device__ __forceinline__ void store_rows_coalesced(float (&x)[32], float *out,
             }
         }
     }
+}
+
+template <int G>
+__device__ __forceinline__ void store_rows_coalesced(float (&x)[4 * G], float *out, int ld, int64_t row0, int col0,
+                                                     int64_t M, int lane) {
+    transpose_groups<G>(x, lane);
+    const int j = lane & (G - 1), g = lane / G;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int64_t row = row0 + 8 * g + k;
+    for (int k = 0; k < G; ++k) {
+        const int64_t row = row0 + G * g + k;
         if (row < M)
             reinterpret_cast<float4 *>(out + row * ld + col0)[j] =
                 make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
     }
+}
+
+template <int G>
+__device__ __forceinline__ void load_rows_coalesced(float (&x)[4 * G], const float *in, int ld, int64_t row0,
+                                                    int col0, int64_t M, int lane) {
+    const int j = lane & (G - 1), g = lane / G;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+        const int64_t row = row0 + G * g + k;
+        const float4 v = row < M ? __ldg(reinterpret_cast<const float4 *>(in + row * ld + col0) + j)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
+    }
+    transpose_groups<G>(x, lane);
 }
 
 template <int BN, int EPI>
@@ -302,41 +326,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // float4 within each 8-lane group so that every store instruction
                     // writes 4 whole 128-byte row segments (one per group) instead of
                     // 32 scattered 16-byte pieces
-                    store_rows_coalesced(x, msg_out, ld_out, (t / n_tiles) * kBM + q * 32, col0, M, lane);
+                    store_rows_coalesced<8>(x, msg_out, ld_out, (t / n_tiles) * kBM + q * 32, col0, M, lane);
                 }
             } else {
                 // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt); this warp: 32 units, 16 at a time
 #pragma unroll 1
                 for (int c = 2 * half; c < 2 * half + 2; ++c) {
+                    const int j0 = nt * 64 + c * 16;
+                    const int64_t row0 = (t / n_tiles) * kBM + q * 32;
+                    float hh[16], o[16];
+                    load_rows_coalesced<4>(hh, gru.h, 128, row0, j0, M, lane);
                     uint32_t vr[16], vz[16], vi[16], vh[16];
                     ptx::tmem_ld16(tbase + 64 + c * 16, vr);
                     ptx::tmem_ld16(tbase + 128 + c * 16, vz);
                     ptx::tmem_ld16(tbase + c * 16, vi);
                     ptx::tmem_ld16(tbase + 192 + c * 16, vh);
                     ptx::tmem_ld_wait();
-                    if (row < M) {
-                        const int j0 = nt * 64 + c * 16;
-                        const float4 *hp = reinterpret_cast<const float4 *>(gru.h + row * 128 + j0);
-                        float4 *op = reinterpret_cast<float4 *>(gru.out + row * 128 + j0);
 #pragma unroll
-                        for (int j4 = 0; j4 < 4; ++j4) {
-                            const float4 hv = __ldg(hp + j4);
-                            const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
-                            float o[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const int j = 4 * j4 + e;
-                                const float rg = sigmoidf_(__uint_as_float(vr[j]) + __ldg(gru.b_ih + j0 + j) +
-                                                           __ldg(gru.b_hh + j0 + j));
-                                const float zg = sigmoidf_(__uint_as_float(vz[j]) + __ldg(gru.b_ih + 128 + j0 + j) +
-                                                           __ldg(gru.b_hh + 128 + j0 + j));
-                                const float n = tanhf_(__uint_as_float(vi[j]) + __ldg(gru.b_ih + 256 + j0 + j) +
-                                                       rg * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
-                                o[e] = (1.0f - zg) * n + zg * hh[e];
-                            }
-                            op[j4] = make_float4(o[0], o[1], o[2], o[3]);
-                        }
+                    for (int j = 0; j < 16; ++j) {
+                        const float rg = sigmoidf_(__uint_as_float(vr[j]) + __ldg(gru.b_ih + j0 + j) +
+                                                   __ldg(gru.b_hh + j0 + j));
+                        const float zg = sigmoidf_(__uint_as_float(vz[j]) + __ldg(gru.b_ih + 128 + j0 + j) +
+                                                   __ldg(gru.b_hh + 128 + j0 + j));
+                        const float n = tanhf_(__uint_as_float(vi[j]) + __ldg(gru.b_ih + 256 + j0 + j) +
+                                               rg * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
+                        o[j] = (1.0f - zg) * n + zg * hh[j];
                     }
+                    store_rows_coalesced<4>(o, gru.out, 128, row0, j0, M, lane);
                 }
             }
             ptx::tc_fence_before();
