@@ -282,6 +282,64 @@ struct GatOp {
         }
         c.m = mb;
     }
+    // Grouped scores (the engine's batch hooks, U = 8): a head's 4 lanes
+    // compute its 8 edge scores two each -- lane 4h + i takes edges i and
+    // i + 4 -- instead of all 8 in every lane, so a batch loads 2 el values
+    // and runs 2 exps per lane instead of 8; the batch max is a 4-lane
+    // reduction and each exp is broadcast to the head's lanes by a shuffle.
+    // Same values in the same order as add_batch (bit-identical).
+    static constexpr bool kGroupScores = true;
+    struct Batch { float el1, el2; };
+    template <int U>
+    __device__ __forceinline__ void load_batch(Val (&v)[U], Batch &b, int32_t cs, int base, int lane) const {
+        static_assert(U == 8, "two edges per lane of a head's 4 lanes");
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t src = __shfl_sync(0xffffffffu, cs, base + u);
+            v[u].z2 = __ldg(reinterpret_cast<const uint32_t *>(
+                ptx::mad_wide((uint32_t)src, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
+        }
+        const int e1 = lane & 3;
+        const int32_t s1 = __shfl_sync(0xffffffffu, cs, base + e1);
+        const int32_t s2 = __shfl_sync(0xffffffffu, cs, base + e1 + 4);
+        const char *elh = reinterpret_cast<const char *>(el) + (lane >> 2) * 4;
+        b.el1 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s1, 32u, elh)));
+        b.el2 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s2, 32u, elh)));
+    }
+    template <int U>
+    __device__ __forceinline__ void add_batch_grouped(Acc &c, const Val (&v)[U], const Batch &b, float er_h,
+                                                      int lane) const {
+        constexpr float kLog2e = 1.4426950408889634f;
+        const float x1 = b.el1 + er_h, x2 = b.el2 + er_h;
+        const float s1 = fmaxf(x1, slope * x1), s2 = fmaxf(x2, slope * x2);  // LeakyReLU, 0 <= slope <= 1
+        float mb = fmaxf(s1, s2);
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+        mb = fmaxf(mb, c.m);
+        const float ml = mb * kLog2e;
+        const float co = ptx::exp2_ftz(fmaf(c.m, kLog2e, -ml));  // 0 when c.m = -inf
+        c.l *= co;
+        c.a0 *= co;
+        c.a1 *= co;
+        const float p1 = ptx::exp2_ftz(fmaf(s1, kLog2e, -ml)), p2 = ptx::exp2_ftz(fmaf(s2, kLog2e, -ml));
+        const int gb = lane & ~3;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float pe = __shfl_sync(0xffffffffu, u < 4 ? p1 : p2, gb | (u & 3));
+            const float2 f = ptx::unpack_bf16x2(v[u].z2);
+            c.l += pe;
+            c.a0 = fmaf(pe, f.x, c.a0);
+            c.a1 = fmaf(pe, f.y, c.a1);
+        }
+        c.m = mb;
+    }
+    // a batch leaving the fast path: every lane takes its head's el of each edge
+    template <int U>
+    __device__ __forceinline__ void unpack_batch(Val (&v)[U], const Batch &b, int lane) const {
+        const int gb = lane & ~3;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u].el = __shfl_sync(0xffffffffu, u < 4 ? b.el1 : b.el2, gb | (u & 3));
+    }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h) const {
         float s = v.el + er_h;
         s = fmaxf(s, slope * s);                 // LeakyReLU for 0 <= slope <= 1
@@ -506,6 +564,18 @@ struct has_batch_add { static constexpr bool value = false; };
 template <typename Op>
 struct has_batch_add<Op, decltype(void(Op::kBatchAdd))> { static constexpr bool value = Op::kBatchAdd; };
 
+// Ops whose batch loads and scores are shared across lanes declare kGroupScores
+// (GatOp: load_batch / add_batch_grouped / unpack_batch and a Batch type).
+template <typename Op, typename = void>
+struct has_group_scores { static constexpr bool value = false; };
+template <typename Op>
+struct has_group_scores<Op, decltype(void(Op::kGroupScores))> { static constexpr bool value = Op::kGroupScores; };
+struct NoBatch {};
+template <typename Op, bool = has_group_scores<Op>::value>
+struct BatchOf { using type = NoBatch; };
+template <typename Op>
+struct BatchOf<Op, true> { using type = typename Op::Batch; };
+
 // Ops that keep a batch split by one row end in registers declare kSplitBatch.
 template <typename Op, typename = void>
 struct has_split_batch { static constexpr bool value = false; };
@@ -531,6 +601,8 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     // across the flush; the others park it (measured per op: GAT +2.5%, C5's
     // 256-wide bf16 rows +40% from the registers held across the flush)
     constexpr bool kSplitBatch = has_split_batch<Op>::value;
+    constexpr bool kGroup = has_group_scores<Op>::value;
+    static_assert(!(kSplitBatch && kGroup), "grouped-score ops park split batches");
     using DW = DenseWarp<U, typename Op::Val, kWinD>;
     __shared__ DW warps[kWarpsPerBlock];
     extern __shared__ float Ws[];  // epilogue operand staged per block: fused-GEMV weight, or bias
@@ -626,11 +698,18 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         slide(q);
         const int base = q - cb;
         typename Op::Val val[U];
+        [[maybe_unused]] typename BatchOf<Op>::type bt;
+        if constexpr (kGroup) {
+            op.template load_batch<U>(val, bt, cs_a, base, lane);
+        } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u) val[u] = op.load(__shfl_sync(kFull, cs_a, base + u), lane);
+            for (int u = 0; u < U; ++u) val[u] = op.load(__shfl_sync(kFull, cs_a, base + u), lane);
+        }
         if (row_end > q + U) {
             // fast path: no row ends inside the batch
-            if constexpr (has_batch_add<Op>::value) {
+            if constexpr (kGroup) {
+                op.template add_batch_grouped<U>(acc, val, bt, rs, lane);
+            } else if constexpr (has_batch_add<Op>::value) {
                 op.template add_batch<U>(acc, val, rs);
             } else {
 #pragma unroll
@@ -665,6 +744,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
             }
         } else {
             // slow path: park the batch, reduce edge by edge
+            if constexpr (kGroup) op.template unpack_batch<U>(val, bt, lane);
 #pragma unroll
             for (int u = 0; u < U; ++u) W.park[u][lane] = val[u];
 #pragma unroll 1
