@@ -182,15 +182,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 16-byte smem stores (one K-major chunk per n).
             if ((reinterpret_cast<uintptr_t>(W) & 15) == 0) {
                 const int units = KB * 8 * (BN / 8);
-                for (int c = et; c < units; c += 128) {
+                auto unit_load = [&](int c, uint4 (&v)[8]) {
                     const int n0 = (c % (BN / 8)) * 8;
-                    const int kc = (c / (BN / 8)) % 8;
-                    const int kb = c / BN;
-                    const int k0 = kb * kBK + kc * 8;
-                    uint4 v[8];
+                    const int k0 = (c / BN) * kBK + ((c / (BN / 8)) % 8) * 8;
 #pragma unroll
                     for (int r = 0; r < 8; ++r)
                         v[r] = __ldg(reinterpret_cast<const uint4 *>(W + (int64_t)(k0 + r) * BN + n0));
+                };
+                auto unit_store = [&](int c, const uint4 (&v)[8]) {
+                    const int n0 = (c % (BN / 8)) * 8;
+                    const int kc = (c / (BN / 8)) % 8;
+                    const int kb = c / BN;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
@@ -205,6 +207,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint8_t *dst = Bs + kb * L::kBBytesPerKB + n * 128 + ((kc ^ (n & 7)) << 4);
                         *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
                     }
+                };
+                // two units per round: 16 loads in flight per thread
+                for (int c = et; c < units; c += 256) {
+                    uint4 va[8], vb[8];
+                    const bool two = c + 128 < units;
+                    unit_load(c, va);
+                    if (two) unit_load(c + 128, vb);
+                    unit_store(c, va);
+                    if (two) unit_store(c + 128, vb);
                 }
             } else {
                 const int chunks = KB * BN * 8;  // 16-byte chunks: (kb, n, kc)
