@@ -256,12 +256,14 @@ def l2_flush_buffer(dev):
     return torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
 
-def cpu_baseline(cfg, d_cpu, og, sample_rows, oracle):
-    """Time the oracle (as it stands) on a bounded row sample on host cores."""
+def cpu_baseline(cfg, d_cpu, og, sample_rows, oracle, reps=1):
+    """Time the oracle (as it stands) on a bounded row sample on host cores
+    (`reps` back-to-back runs of it)."""
     t0 = time.perf_counter()
-    harness_step_rows(cfg, og, d_cpu, sample_rows, oracle)
+    for _ in range(reps):
+        harness_step_rows(cfg, og, d_cpu, sample_rows, oracle)
     dt = time.perf_counter() - t0
-    upd = sample_updates(cfg, og, sample_rows)
+    upd = sample_updates(cfg, og, sample_rows) * reps
     return upd / dt, dt, upd
 
 
@@ -472,9 +474,22 @@ def run_saga(args, cfg):
         og = oracle.csr_build(cfg.n, c["src"], c["dst"], c.get("etype"), cfg.num_etypes)
         rows = pick_sample(og, args.ref_edges)
         v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
+        # grow the sample to about --ref-seconds of CPU work: more rows, up to
+        # the whole graph, then repeated runs of it
+        reps = 1
+        if args.ref_seconds > 0 and dt < 0.5 * args.ref_seconds:
+            e_all = int(og.in_deg.sum())
+            want = int(upd / cfg.f_canon * args.ref_seconds / max(dt, 1e-4))
+            if cfg.model != "sage" and want > 1.5 * upd / cfg.f_canon and len(rows) < og.n:
+                rows = pick_sample(og, min(want, e_all))
+                v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
+            if dt < 0.5 * args.ref_seconds:
+                reps = int(min(100000, max(1, args.ref_seconds / max(dt, 1e-5))))
+                v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle, reps)
+        per = upd // reps // cfg.f_canon
         cpu = {"value": v_cpu, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
-               "sample": f"{len(rows)} random destination rows of {cfg.name} ({upd // cfg.f_canon} in-edges), "
-                         f"fp64 C oracle, {dt:.1f} s"}
+               "sample": f"{len(rows)} random destination rows of {cfg.name} ({per} in-edges)"
+                         + (f" x {reps} runs" if reps > 1 else "") + f", fp64 C oracle, {dt:.1f} s"}
 
     conf = workload_config(cfg)
     conf.update({"l2": "inputs larger than L2 (no flush)" if big else "512 MiB L2 flush between steps (untimed)",
@@ -575,6 +590,8 @@ def main():
                     help="SAGE (C2): Gather fused with the concat-GEMM in one kernel (NEXT-1)")
     ap.add_argument("--ref-edges", type=int, default=2_000_000,
                     help="in-edges per oracle sample (bounded CPU work)")
+    ap.add_argument("--ref-seconds", type=float, default=10.0,
+                    help="cpu_baseline: grow the oracle's row sample to about this much CPU time")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="diagnostic: no per-kernel event pairs in the timed graph (no roofline)")
