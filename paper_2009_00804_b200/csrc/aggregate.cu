@@ -473,6 +473,24 @@ struct EdgeMlpOp {
         return Val{__ldg(reinterpret_cast<const float4 *>(
             ptx::mad_wide((uint32_t)u, 1024u, reinterpret_cast<const char *>(AB) + lane * 16)))};
     }
+    // fast path: the batch's messages reduced in fp32 (sum of U terms, or the
+    // exact max), then one fp64 update per element -- as SumF32Op
+    static constexpr bool kBatchAdd = true;
+    template <int U>
+    __device__ __forceinline__ void add_batch(Acc &c, const Val (&v)[U], float) const {
+        float s[4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float y[4] = {v[u].x.x + c.b.x, v[u].x.y + c.b.y, v[u].x.z + c.b.z, v[u].x.w + c.b.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (kRelu) y[i] = fmaxf(y[i], 0.0f);
+                s[i] = u == 0 ? y[i] : (kMax ? fmaxf(s[i], y[i]) : s[i] + y[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.a[i] = kMax ? fmax(c.a[i], (double)s[i]) : c.a[i] + (double)s[i];
+    }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float) const {
         float y[4] = {v.x.x + c.b.x, v.x.y + c.b.y, v.x.z + c.b.z, v.x.w + c.b.w};
 #pragma unroll
