@@ -584,7 +584,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5", choices=sorted(W.CONFIGS))
     ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly (no CUDA graph)")
     ap.add_argument("--sage-fused", action="store_true",
                     help="SAGE (C2): Gather fused with the concat-GEMM in one kernel (NEXT-1)")
