@@ -202,6 +202,28 @@ struct GcnF32FusedOp {
         float h[NPL];
 #pragma unroll
         for (int i = 0; i < NPL; ++i) h[i] = (float)((double)rs * c.a[i]);
+        if (f_out <= 16) {
+            // narrow outputs (C1: 64 -> 16): lane = (k half, column); each half
+            // runs its own dependent FMA chains over half the inputs (one per
+            // NPL slot), folded by one shuffle -- a quarter of the chain length
+            const int j = lane & 15, kh = lane >> 4, nk = f_in / NPL;
+            float o[NPL];
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) o[i] = 0.0f;
+            for (int kl = kh * (nk / 2); kl < (kh + 1) * (nk / 2); ++kl) {
+#pragma unroll
+                for (int i = 0; i < NPL; ++i) {
+                    const float hk = __shfl_sync(kFull, h[i], kl);
+                    if (j < f_out) o[i] = fmaf(hk, Ws[(kl * NPL + i) * f_out + j], o[i]);
+                }
+            }
+            float acc = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) acc += o[i];
+            acc += __shfl_xor_sync(kFull, acc, 16);
+            if (kh == 0 && j < f_out) out[(int64_t)v * f_out + j] = act_fn(acc + (bias ? __ldg(bias + j) : 0.0f), act);
+            return;
+        }
         float o0 = 0.0f, o1 = 0.0f;
         const int j0 = lane, j1 = lane + 32;
         for (int kl = 0; kl < f_in / NPL; ++kl) {  // lane kl holds inputs kl*NPL ..
