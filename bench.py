@@ -267,6 +267,28 @@ def cpu_baseline(cfg, d_cpu, og, sample_rows, oracle, reps=1):
     return upd / dt, dt, upd
 
 
+def sized_cpu_baseline(cfg, c, og, oracle, ref_edges, ref_seconds):
+    """The cpu_baseline object: the oracle timed on a row sample of about
+    ref_edges in-edges, grown to about ref_seconds of CPU work (more rows, up
+    to the whole graph, then back-to-back repeated runs of it)."""
+    rows = pick_sample(og, ref_edges)
+    v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
+    reps = 1
+    if ref_seconds > 0 and dt < 0.5 * ref_seconds:
+        e_all = int(og.in_deg.sum())
+        want = int(upd / cfg.f_canon * ref_seconds / max(dt, 1e-4))
+        if cfg.model != "sage" and want > 1.5 * upd / cfg.f_canon and len(rows) < og.n:
+            rows = pick_sample(og, min(want, e_all))
+            v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
+        if dt < 0.5 * ref_seconds:
+            reps = int(min(100000, max(1, ref_seconds / max(dt, 1e-5))))
+            v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle, reps)
+    per = upd // reps // cfg.f_canon
+    return {"value": v_cpu, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+            "sample": f"{len(rows)} random destination rows of {cfg.name} ({per} in-edges)"
+                      + (f" x {reps} runs" if reps > 1 else "") + f", fp64 C oracle, {dt:.1f} s"}
+
+
 def harness_step_rows(cfg, og, c, rows, oracle):
     """The oracle's configured step restricted to destination `rows`
     (SAGE: both layers over all rows -- layer 2 needs H1 of every neighbour)."""
@@ -472,24 +494,7 @@ def run_saga(args, cfg):
         import oracle
         c = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in d.items()}
         og = oracle.csr_build(cfg.n, c["src"], c["dst"], c.get("etype"), cfg.num_etypes)
-        rows = pick_sample(og, args.ref_edges)
-        v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
-        # grow the sample to about --ref-seconds of CPU work: more rows, up to
-        # the whole graph, then repeated runs of it
-        reps = 1
-        if args.ref_seconds > 0 and dt < 0.5 * args.ref_seconds:
-            e_all = int(og.in_deg.sum())
-            want = int(upd / cfg.f_canon * args.ref_seconds / max(dt, 1e-4))
-            if cfg.model != "sage" and want > 1.5 * upd / cfg.f_canon and len(rows) < og.n:
-                rows = pick_sample(og, min(want, e_all))
-                v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle)
-            if dt < 0.5 * args.ref_seconds:
-                reps = int(min(100000, max(1, args.ref_seconds / max(dt, 1e-5))))
-                v_cpu, dt, upd = cpu_baseline(cfg, c, og, rows, oracle, reps)
-        per = upd // reps // cfg.f_canon
-        cpu = {"value": v_cpu, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
-               "sample": f"{len(rows)} random destination rows of {cfg.name} ({per} in-edges)"
-                         + (f" x {reps} runs" if reps > 1 else "") + f", fp64 C oracle, {dt:.1f} s"}
+        cpu = sized_cpu_baseline(cfg, c, og, oracle, args.ref_edges, args.ref_seconds)
 
     conf = workload_config(cfg)
     conf.update({"l2": "inputs larger than L2 (no flush)" if big else "512 MiB L2 flush between steps (untimed)",

@@ -94,3 +94,18 @@ def test_lstm_gather_is_held_to_the_fma_pipe(bench):
     assert r["bound"] == "alu" and r["unit"] == "TFLOP/s"
     assert abs(r["peak"] - 148 * 4 * 16 * 2 * 1.965e9 / 1e12) < 1e-9
     assert r["achieved"] == pytest.approx(a["flops"] / 5.0e-3 / 1e12)
+
+
+def test_cpu_baseline_sample_grows_to_the_time_target(bench):
+    """cpu_baseline sizing: a tiny first sample is grown (whole graph, then
+    repeated runs) to about the requested CPU time; the value is updates/s of
+    the oracle as it stands."""
+    import oracle
+    c = W.scaled(W.CONFIGS["C1"], 256, 1024, "C1t")
+    d = W.make_inputs(c, "cpu")
+    og = oracle.csr_build(c.n, d["src"], d["dst"])
+    cpu = bench.sized_cpu_baseline(c, d, og, oracle, ref_edges=64, ref_seconds=0.2)
+    assert cpu["kind"] == "oracle" and cpu["value"] > 0 and cpu["cores"] >= 1
+    assert f"{c.n} random destination rows" in cpu["sample"] and " runs" in cpu["sample"]
+    none = bench.sized_cpu_baseline(c, d, og, oracle, ref_edges=64, ref_seconds=0)
+    assert " runs" not in none["sample"]
