@@ -172,8 +172,8 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  * normalisation and split reductions, which changes only rounding):
  *  GCN   (Table 1; BASELINE.json C1/C5; A1, A2, A12):
  *        out[v] = act( sum_{u->v} deg(u)^-1/2 deg(v)^-1/2 x[u] . W + bias )
- *        features F32 (fused aggregate + SIMT GEMV, in_dim % 4 == 0, <= 128,
- *        out_dim <= 64) or BF16 (tcgen05 GEMM first, then aggregation;
+ *        features F32 (fused aggregate + SIMT GEMV, in_dim in {16, 32, 64, 128},
+ *        1 <= out_dim <= 64) or BF16 (tcgen05 GEMM first, then aggregation;
  *        in_dim in {64,128,192,256}, out_dim in {64,128,256}).
  *  SAGE  (Table 1; BASELINE.json C2; A11, A12):
  *        out[v] = act( [x[v] || mean_{u->v} x[u]] . W + bias ), W [2*in][out]
@@ -186,6 +186,11 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *  GATED (lines 142-147, Table 1; BASELINE.json C4; A6, A15, A16):
  *        m[v] = sum_{u->v} x[u] . W_type[t(u->v)]; out[v] = GRUCell(m[v], x[v])
  *        F32, in_dim = out_dim = 128, num_etypes <= 4.
+ *        Precision (GATED and GGNN): the message / GRU GEMMs run as split-TF32
+ *        (22-bit operands, fp32 tensor-core accumulation) for rows with
+ *        in-degree < 256; rows with in-degree >= 256, whose summed message
+ *        grows with the in-degree, are recomputed with fp64 products, sums and
+ *        nonlinearities from the fp32-stored S / m ("Precision").
  *  SAGE_LSTM (Table 1; A25):
  *        h[v] = final state of LSTMCell(W_ih, W_hh, b_ih, b_hh) run over x[u]
  *        for v's in-edges u -> v in CSR order from a zero state (0 without
@@ -213,7 +218,11 @@ SAGA_API saga_status saga_layer(saga_model kind, const saga_graph *g, const saga
                        const saga_weights *w, saga_tensor *out, const saga_layer_opts *opts,
                        void *workspace, size_t workspace_bytes, void *cuda_stream);
 
-/* Release a graph (stream-ordered on the stream it was built on). NULL-safe. */
+/* Release a graph.  NULL-safe.  The device arrays are freed stream-ordered
+ * on the stream the graph was BUILT on (cudaFreeAsync); the caller must make
+ * sure that work on any OTHER stream that reads the graph has completed (or
+ * is ordered before that stream, e.g. by an event) -- the Python Graph.close()
+ * synchronises the device first.  The build stream must still exist. */
 SAGA_API void saga_free(saga_graph *g);
 
 /*

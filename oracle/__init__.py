@@ -259,3 +259,26 @@ def rel_err(y, y_ref) -> float:
     den = float(np.max(np.abs(y_ref))) if y_ref.size else 0.0
     num = float(np.max(np.abs(y - y_ref))) if y.size else 0.0
     return num / den if den > 0 else num
+
+
+def row_err(y, y_ref, floor=1e-3):
+    """Per-row diagnostic of SURVEY.md 8(c) (the "Error metric" row):
+    max over rows v of ||y_v - yref_v||_inf / max(||yref_v||_inf, floor * ||yref||_inf).
+
+    Returns (worst value, index of the worst row).  A row that is badly wrong
+    but small next to the tensor's largest row shows up here and not in
+    rel_err.  NaN/Inf anywhere -> (inf, -1); an empty tensor -> (0, -1)."""
+    y = np.asarray(y, dtype=np.float64)
+    y_ref = np.asarray(y_ref, dtype=np.float64)
+    if not np.all(np.isfinite(y)):
+        return float("inf"), -1
+    if y_ref.size == 0:
+        return 0.0, -1
+    y2, r2 = y.reshape(y.shape[0], -1), y_ref.reshape(y_ref.shape[0], -1)
+    glob = float(np.max(np.abs(r2)))
+    if glob == 0.0:
+        num = np.max(np.abs(y2 - r2), axis=1)
+        return float(num.max()), int(num.argmax())
+    den = np.maximum(np.max(np.abs(r2), axis=1), floor * glob)
+    e = np.max(np.abs(y2 - r2), axis=1) / den
+    return float(e.max()), int(e.argmax())

@@ -155,7 +155,10 @@ class Graph:
         self.num_vertices, self.num_edges, self.num_etypes = n, e, t
 
     def close(self):
+        """saga_free is stream-ordered on the BUILD stream only (saga.h): layers
+        may have used the graph on other streams, so wait for the device first."""
         if self.handle:
+            torch.cuda.synchronize()
             saga_free(self)
             self.handle = None
 

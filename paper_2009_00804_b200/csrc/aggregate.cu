@@ -416,7 +416,22 @@ struct SumF32Op {
     const float *H;
     const float *scale;  // nullptr: plain sum
     float *S;
-    __device__ __forceinline__ float row_value(int32_t r, int) const { return scale ? __ldg(scale + r) : 1.0f; }
+    // gated layer: the heavy rows' sums (in-degree >= kHeavyInDeg) also in fp64,
+    // Sx[slot][t][128], for the fp64 ApplyVertex (gru_f64.cu); nullptr: none
+    const int32_t *hslot;
+    double *Sx;
+    int32_t T;
+    // Row value (read through the engine's 32-row window, never a dependent
+    // load in the row flush): the mean's 1/|row|, or for the plain sum 1, or
+    // -(slot + 1) for a heavy row (its fp64 copy goes to Sx[slot]).
+    __device__ __forceinline__ float row_value(int32_t r, int) const {
+        if (scale) return __ldg(scale + r);
+        if (Sx) {
+            const int32_t hs = __ldg(hslot + r / T);
+            return hs >= 0 ? -(float)(hs + 1) : 1.0f;
+        }
+        return 1.0f;
+    }
     __device__ __forceinline__ void zero(Acc &c) const {
 #pragma unroll
         for (int i = 0; i < 4; ++i) c.a[i] = 0.0;
@@ -448,9 +463,15 @@ struct SumF32Op {
         c.a[3] += (double)v.x.w;
     }
     __device__ __forceinline__ void finish(int32_t r, const Acc &c, float rs, int lane, const float *) const {
-        const double d = (double)rs;
+        const double d = rs < 0.0f ? 1.0 : (double)rs;
         reinterpret_cast<float4 *>(S + (int64_t)r * 128)[lane] =
             make_float4((float)(c.a[0] * d), (float)(c.a[1] * d), (float)(c.a[2] * d), (float)(c.a[3] * d));
+        if (rs < 0.0f) {  // heavy row: also the fp64 sums
+            const int64_t hs = (int64_t)(-rs) - 1;
+            double2 *x = reinterpret_cast<double2 *>(Sx + (hs * T + r % T) * 128) + lane * 2;
+            x[0] = make_double2(c.a[0], c.a[1]);
+            x[1] = make_double2(c.a[2], c.a[3]);
+        }
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
         double2 *d = reinterpret_cast<double2 *>(slot) + lane * 2;
@@ -478,16 +499,21 @@ struct EdgeMlpOp {
     static constexpr int kWin = 0;
     static constexpr int kSlot = 2 * 32 * 4;  // doubles as float pairs
     __device__ static int win_col(int) { return 0; }
-    struct Acc { double a[4]; float4 b; };
+    // hs: the row's heavy slot (>= 0: in-degree >= kHeavyInDeg) -- warp-uniform
+    struct Acc { double a[4]; float4 b; int32_t hs; };
     struct Val { float4 x; };
-    const float *AB;  // [n][256]
-    float *m;         // [n][128]
+    const float *AB;       // [n][256]
+    float *m;              // [n][128]
+    const int32_t *hslot;  // [n] heavy slot or -1 (GraphDev::heavy_slot)
+    const double *Bx;      // [n_heavy][128] B of the heavy rows in fp64 (gru_f64.cu)
+    double *mx;            // [n_heavy][128] m of the heavy rows, never rounded to fp32
     __device__ __forceinline__ float row_value(int32_t, int) const { return 0.0f; }
     __device__ __forceinline__ void zero(Acc &c) const {
 #pragma unroll
         for (int i = 0; i < 4; ++i) c.a[i] = kMax ? -INFINITY : 0.0;
     }
     __device__ __forceinline__ void begin_row(Acc &c, int32_t v, int lane) const {
+        c.hs = __ldg(hslot + v);
         c.b = __ldg(reinterpret_cast<const float4 *>(
             ptx::mad_wide((uint32_t)v, 1024u, reinterpret_cast<const char *>(AB) + 512 + lane * 16)));
     }
@@ -495,11 +521,34 @@ struct EdgeMlpOp {
         return Val{__ldg(reinterpret_cast<const float4 *>(
             ptx::mad_wide((uint32_t)u, 1024u, reinterpret_cast<const char *>(AB) + lane * 16)))};
     }
+    // Heavy rows (in-degree >= kHeavyInDeg) add their fp64 B[v] to every
+    // in-edge's A[u] in fp64: B[v] enters the sum deg(v) times, so the tensor
+    // GEMM's fp32 B (error ~1e-7) would be amplified by the in-degree into m.
+    __device__ __forceinline__ void add_heavy(Acc &c, const float4 &x, const double (&bd)[4]) const {
+        const double y[4] = {(double)x.x + bd[0], (double)x.y + bd[1], (double)x.z + bd[2], (double)x.w + bd[3]};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double t = kRelu ? fmax(y[i], 0.0) : y[i];
+            c.a[i] = kMax ? fmax(c.a[i], t) : c.a[i] + t;
+        }
+    }
+    __device__ __forceinline__ void load_bd(double (&bd)[4], int32_t hs, int lane) const {
+        const double2 *bp = reinterpret_cast<const double2 *>(Bx + (int64_t)hs * 128) + lane * 2;
+        const double2 b0 = __ldg(bp), b1 = __ldg(bp + 1);
+        bd[0] = b0.x; bd[1] = b0.y; bd[2] = b1.x; bd[3] = b1.y;
+    }
     // fast path: the batch's messages reduced in fp32 (sum of U terms, or the
     // exact max), then one fp64 update per element -- as SumF32Op
     static constexpr bool kBatchAdd = true;
     template <int U>
     __device__ __forceinline__ void add_batch(Acc &c, const Val (&v)[U], float) const {
+        if (c.hs >= 0) {
+            double bd[4];
+            load_bd(bd, c.hs, threadIdx.x & 31);
+#pragma unroll
+            for (int u = 0; u < U; ++u) add_heavy(c, v[u].x, bd);
+            return;
+        }
         float s[4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -514,6 +563,12 @@ struct EdgeMlpOp {
         for (int i = 0; i < 4; ++i) c.a[i] = kMax ? fmax(c.a[i], (double)s[i]) : c.a[i] + (double)s[i];
     }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float) const {
+        if (c.hs >= 0) {
+            double bd[4];
+            load_bd(bd, c.hs, threadIdx.x & 31);
+            add_heavy(c, v.x, bd);
+            return;
+        }
         float y[4] = {v.x.x + c.b.x, v.x.y + c.b.y, v.x.z + c.b.z, v.x.w + c.b.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -525,10 +580,16 @@ struct EdgeMlpOp {
         }
     }
     __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
-        float o[4];
+        double o[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = (kMax && c.a[i] == -INFINITY) ? 0.0f : (float)c.a[i];
-        reinterpret_cast<float4 *>(m + (int64_t)v * 128)[lane] = make_float4(o[0], o[1], o[2], o[3]);
+        for (int i = 0; i < 4; ++i) o[i] = (kMax && c.a[i] == -INFINITY) ? 0.0 : c.a[i];
+        reinterpret_cast<float4 *>(m + (int64_t)v * 128)[lane] =
+            make_float4((float)o[0], (float)o[1], (float)o[2], (float)o[3]);
+        if (c.hs >= 0) {  // (a merged split row gets begin_row in ticket_merge too)
+            double2 *d = reinterpret_cast<double2 *>(mx + (int64_t)c.hs * 128) + lane * 2;
+            d[0] = make_double2(o[0], o[1]);
+            d[1] = make_double2(o[2], o[3]);
+        }
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
         double2 *d = reinterpret_cast<double2 *>(slot) + lane * 2;
@@ -544,18 +605,6 @@ struct EdgeMlpOp {
     }
 };
 
-// Ops that carry per-row state loaded at the row's start implement begin_row.
-template <typename Op, typename = void>
-struct has_begin_row { static constexpr bool value = false; };
-template <typename Op>
-struct has_begin_row<Op, decltype(void(&Op::begin_row))> { static constexpr bool value = true; };
-template <typename Op>
-__device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, int32_t v, int32_t n, int lane) {
-    if constexpr (has_begin_row<Op>::value) {
-        if (v < n) op.begin_row(c, v, lane);
-    }
-}
-
 // Ops whose epilogue needs the whole warp (the fused GEMV) implement finish_w.
 template <typename Op>
 __device__ __forceinline__ auto do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int lane,
@@ -566,6 +615,18 @@ template <typename Op>
 __device__ __forceinline__ void do_finish(const Op &op, int32_t v, const typename Op::Acc &c, float rs, int lane,
                                           const float *Ws, long) {
     op.finish(v, c, rs, lane, Ws);
+}
+
+// Ops that carry per-row state loaded at the row's start implement begin_row.
+template <typename Op, typename = void>
+struct has_begin_row { static constexpr bool value = false; };
+template <typename Op>
+struct has_begin_row<Op, decltype(void(&Op::begin_row))> { static constexpr bool value = true; };
+template <typename Op>
+__device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, int32_t v, int32_t n, int lane) {
+    if constexpr (has_begin_row<Op>::value) {
+        if (v < n) op.begin_row(c, v, lane);
+    }
 }
 
 // Split rows (hubs, rows straddling a task boundary): every task holding part
@@ -591,6 +652,7 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
         if (lane == 0) ws.counters[k2] = 0;  // every contributor has taken its ticket: leave it zero
         typename Op::Acc m;
         op.zero(m);
+        begin_row_of(op, m, r, r + 1, lane);  // per-row state the epilogue may read
         op.merge(m, ws.partials + (2 * k1 + 1) * Op::kSlot, lane);
         for (int64_t kk = k1 + 1; kk <= k2; ++kk) op.merge(m, ws.partials + (2 * kk) * Op::kSlot, lane);
         const float rs = Op::kWin ? op.row_value(r, Op::win_col(lane)) : 0.0f;
@@ -943,25 +1005,27 @@ cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const flo
     return run<8, 5>(view_fine(g), op, ws, st);  // 48 registers, 40 warps per SM: 3% faster than 4 blocks
 }
 
-cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,
-                                 cudaStream_t st) {
+cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, double *Sx,
+                                 AggWorkspace ws, cudaStream_t st) {
     if (f != 128) return cudaErrorInvalidValue;
     const GraphView gv = g.trow_ptr ? view_typed(g) : view(g);  // no edge types: T = 1
-    SumF32Op op{H, mean ? (g.trow_ptr ? g.tinv_deg : g.inv_deg) : nullptr, S};
+    SumF32Op op{H, mean ? (g.trow_ptr ? g.tinv_deg : g.inv_deg) : nullptr, S, g.heavy_slot, Sx,
+                g.trow_ptr ? g.num_etypes : 1};
     // U = 4 at 64 registers: measured 3-4% faster than U = 8 (C4, C6), and
     // U = 8 needs more registers (spills at 64, 15% slower at 3 blocks/SM)
     return run<4, 4>(gv, op, ws, st);
 }
 
 cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t f, bool relu, bool max, float *m,
-                                    AggWorkspace ws, cudaStream_t st) {
+                                    const double *Bx, double *mx, AggWorkspace ws, cudaStream_t st) {
     if (f != 128) return cudaErrorInvalidValue;
+    const int32_t *hs = g.heavy_slot;
     if (max) {
-        if (relu) return run<4, 4>(view(g), EdgeMlpOp<true, true>{AB, m}, ws, st);
-        return run<4, 4>(view(g), EdgeMlpOp<true, false>{AB, m}, ws, st);
+        if (relu) return run<4, 4>(view(g), EdgeMlpOp<true, true>{AB, m, hs, Bx, mx}, ws, st);
+        return run<4, 4>(view(g), EdgeMlpOp<true, false>{AB, m, hs, Bx, mx}, ws, st);
     }
-    if (relu) return run<4, 4>(view(g), EdgeMlpOp<false, true>{AB, m}, ws, st);
-    return run<4, 4>(view(g), EdgeMlpOp<false, false>{AB, m}, ws, st);
+    if (relu) return run<4, 4>(view(g), EdgeMlpOp<false, true>{AB, m, hs, Bx, mx}, ws, st);
+    return run<4, 4>(view(g), EdgeMlpOp<false, false>{AB, m, hs, Bx, mx}, ws, st);
 }
 
 bool gcn_f32_rowwise(const GraphDev &g) { return g.max_in_deg <= kRowwiseMaxDeg; }

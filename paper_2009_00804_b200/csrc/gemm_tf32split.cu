@@ -41,6 +41,7 @@
 #include <cstdint>
 #include <mutex>
 
+#include "epilogue.cuh"
 #include "internal.cuh"
 #include "ptx.cuh"
 
@@ -96,65 +97,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // of every row; with IEEE division and tanhf it was the kernel's bound.
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanhf_(float x) { return 2.0f * sigmoidf_(2.0f * x) - 1.0f; }
-
-// Row-per-lane tiles <-> coalesced row segments.  A warp holds rows row0 + lane
-// (lane 0..31) of a [M][ld] fp32 matrix, G float4 (columns col0 .. col0+4G-1)
-// per lane in x[4G].  transpose_groups<G> transposes each G-lane group's G x G
-// block of float4 with log2(G) butterfly stages (shfl_xor 1, 2, 4): afterwards
-// lane j of group g holds float4 j of rows G g .. G g + G-1 (slot k = row G g + k);
-// it is its own inverse.  The store / load below then move whole 16G-byte row
-// segments per instruction (32/G rows each) instead of 32 scattered 16-byte
-// pieces.  Rows >= M are skipped (loads give 0).
-template <int G>
-__device__ __forceinline__ void transpose_groups(float (&x)[4 * G], int lane) {
-    const int j = lane & (G - 1);
-#pragma unroll
-    for (int s = 1; s < G; s <<= 1) {
-        const bool hi = (j & s) != 0;
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-            if (k & s) continue;
-            // the slot of the pair (k, k|s) whose bit s differs from the lane's
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float send = hi ? x[4 * k + e] : x[4 * (k | s) + e];
-                const float recv = __shfl_xor_sync(0xffffffffu, send, s);
-                if (hi)
-                    x[4 * k + e] = recv;
-                else
-                    x[4 * (k | s) + e] = recv;
-            }
-        }
-    }
-}
-
-template <int G>
-__device__ __forceinline__ void store_rows_coalesced(float (&x)[4 * G], float *out, int ld, int64_t row0, int col0,
-                                                     int64_t M, int lane) {
-    transpose_groups<G>(x, lane);
-    const int j = lane & (G - 1), g = lane / G;
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-        const int64_t row = row0 + G * g + k;
-        if (row < M)
-            reinterpret_cast<float4 *>(out + row * ld + col0)[j] =
-                make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
-    }
-}
-
-template <int G>
-__device__ __forceinline__ void load_rows_coalesced(float (&x)[4 * G], const float *in, int ld, int64_t row0,
-                                                    int col0, int64_t M, int lane) {
-    const int j = lane & (G - 1), g = lane / G;
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-        const int64_t row = row0 + G * g + k;
-        const float4 v = row < M ? __ldg(reinterpret_cast<const float4 *>(in + row * ld + col0) + j)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
-    }
-    transpose_groups<G>(x, lane);
-}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -326,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // float4 within each 8-lane group so that every store instruction
                     // writes 4 whole 128-byte row segments (one per group) instead of
                     // 32 scattered 16-byte pieces
-                    store_rows_coalesced<8>(x, msg_out, ld_out, (t / n_tiles) * kBM + q * 32, col0, M, lane);
+                    epi::store_rows_coalesced<8>(x, msg_out, ld_out, (t / n_tiles) * kBM + q * 32, col0, M, lane);
                 }
             } else {
                 // tile columns: [gin | r | z | ghn] x 64 units (unit0 = 64 nt); this warp: 32 units, 16 at a time
@@ -335,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int j0 = nt * 64 + c * 16;
                     const int64_t row0 = (t / n_tiles) * kBM + q * 32;
                     float hh[16], o[16];
-                    load_rows_coalesced<4>(hh, gru.h, 128, row0, j0, M, lane);
+                    epi::load_rows_coalesced<4>(hh, gru.h, 128, row0, j0, M, lane);
                     uint32_t vr[16], vz[16], vi[16], vh[16];
                     ptx::tmem_ld16(tbase + 64 + c * 16, vr);
                     ptx::tmem_ld16(tbase + 128 + c * 16, vz);
@@ -352,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                rg * (__uint_as_float(vh[j]) + __ldg(gru.b_hh + 256 + j0 + j)));
                         o[j] = (1.0f - zg) * n + zg * hh[j];
                     }
-                    store_rows_coalesced<4>(o, gru.out, 128, row0, j0, M, lane);
+                    epi::store_rows_coalesced<4>(o, gru.out, 128, row0, j0, M, lane);
                 }
             }
             ptx::tc_fence_before();
@@ -561,27 +503,13 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
 
 size_t ggnn_tc_workspace_floats(int32_t f) { return (size_t)2 * 2 * f * f + 2 * f + (size_t)2 * 4 * f * 2 * f; }
 
-cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e,
-                                const float *W_ih, const float *W_hh, float *wsplit, float *AB, cudaStream_t st,
-                                const char **why) {
-    if (M == 0) return cudaSuccess;
-    if (f != 128) {
-        *why = "tensor-core GGNN path needs f = 128";
-        return cudaErrorInvalidValue;
-    }
+// GGNN (NEXT-4): the GRU's split B^T (the edge-MLP projection AB runs on the
+// int8-sliced exact-accumulation GEMM, gemm_i8x.cu).
+cudaError_t launch_ggnn_split_weights(int32_t f, const float *W_e, const float *b_e, const float *W_ih,
+                                      const float *W_hh, float *wsplit, cudaStream_t st) {
     float *be_hi = wsplit, *be_lo = be_hi + (size_t)2 * f * f, *bias2 = be_lo + (size_t)2 * f * f;
     float *bg_hi = bias2 + 2 * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
-    cudaError_t e = launch<false>(k_split_ggnn, 256, 256, 0, st, f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
-    if (e) return e;
-    CUtensorMap aH, bh, bl;
-    if (!make_map_f32(&aH, H, M, f, f, kBM) || !make_map_f32(&bh, be_hi, 2 * f, f, f, 128) ||
-        !make_map_f32(&bl, be_lo, 2 * f, f, f, 128)) {
-        *why = "cuTensorMapEncodeTiled failed";
-        return cudaErrorInvalidValue;
-    }
-    // AB = H . [W_a | W_b] + [0 | b_e]: two 128-column tiles
-    GruEpi epi{nullptr, nullptr, nullptr, nullptr, bias2, 0};
-    return launch_tf32split<128, EPI_MSG>(aH, aH, bh, bl, M, f / kBK, f / kBK, 2, AB, 2 * f, epi, st);
+    return launch<false>(k_split_ggnn, 256, 256, 0, st, f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
 }
 
 cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float *H, const float *b_ih,

@@ -53,12 +53,22 @@ __global__ void k_range_degrees(int32_t n, int64_t e, const int32_t *__restrict_
 }
 
 // max in-degree (read back with the range-check result)
+// max in-degree and the number of heavy rows (in-degree >= kHeavyInDeg), read
+// back with the range check
 __global__ void k_max_deg(int32_t n, const int32_t *__restrict__ in_deg, unsigned long long *out) {
-    int32_t m = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    int32_t m = 0, heavy = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         m = max(m, in_deg[i]);
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+        heavy += in_deg[i] >= kHeavyInDeg;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        heavy += __shfl_xor_sync(0xffffffffu, heavy, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, (unsigned long long)m);
+        if (heavy) atomicAdd(out + 1, (unsigned long long)heavy);
+    }
 }
 
 // ------------------------------------------------------------------- scan ----
@@ -142,16 +152,18 @@ cudaError_t scan_exclusive(const Tin *in, int64_t count, int64_t *out, cudaStrea
     }
     int64_t *sums = nullptr, *offs = nullptr;
     cudaError_t err = cudaMallocAsync(&sums, sizeof(int64_t) * tiles, st);
-    if (err) return err;
-    err = cudaMallocAsync(&offs, sizeof(int64_t) * (tiles + 1), st);
-    if (err) return err;
-    k_scan_tile_sums<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, sums);
-    err = scan_exclusive<int64_t>(sums, tiles, offs, st);
-    if (err) return err;
-    k_scan_tiles<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, offs, out);
-    cudaFreeAsync(sums, st);
-    cudaFreeAsync(offs, st);
-    return cudaGetLastError();
+    if (!err) err = cudaMallocAsync(&offs, sizeof(int64_t) * (tiles + 1), st);
+    if (!err) {
+        k_scan_tile_sums<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, sums);
+        err = scan_exclusive<int64_t>(sums, tiles, offs, st);
+    }
+    if (!err) {
+        k_scan_tiles<Tin><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, count, offs, out);
+        err = cudaGetLastError();
+    }
+    if (sums) cudaFreeAsync(sums, st);  // every buffer allocated so far, also on failure
+    if (offs) cudaFreeAsync(offs, st);
+    return err;
 }
 
 // ------------------------------------------------------------- radix sort ----
@@ -291,15 +303,14 @@ static cudaError_t radix_sort_index(const int32_t *keys, int64_t count, int key_
         return cudaGetLastError();
     }
     const int64_t nblocks = (count + kSortTile - 1) / kSortTile;
-    int32_t *kbuf[2], *vbuf[2], *hist;
-    int64_t *offs;
-    cudaError_t err;
-    if ((err = cudaMallocAsync(&kbuf[0], sizeof(int32_t) * count, st))) return err;
-    if ((err = cudaMallocAsync(&kbuf[1], sizeof(int32_t) * count, st))) return err;
-    if ((err = cudaMallocAsync(&vbuf[0], sizeof(int32_t) * count, st))) return err;
-    if ((err = cudaMallocAsync(&vbuf[1], sizeof(int32_t) * count, st))) return err;
-    if ((err = cudaMallocAsync(&hist, sizeof(int32_t) * kRadix * nblocks, st))) return err;
-    if ((err = cudaMallocAsync(&offs, sizeof(int64_t) * (kRadix * nblocks + 1), st))) return err;
+    int32_t *kbuf[2] = {nullptr, nullptr}, *vbuf[2] = {nullptr, nullptr}, *hist = nullptr;
+    int64_t *offs = nullptr;
+    cudaError_t err = cudaMallocAsync(&kbuf[0], sizeof(int32_t) * count, st);
+    if (!err) err = cudaMallocAsync(&kbuf[1], sizeof(int32_t) * count, st);
+    if (!err) err = cudaMallocAsync(&vbuf[0], sizeof(int32_t) * count, st);
+    if (!err) err = cudaMallocAsync(&vbuf[1], sizeof(int32_t) * count, st);
+    if (!err) err = cudaMallocAsync(&hist, sizeof(int32_t) * kRadix * nblocks, st);
+    if (!err) err = cudaMallocAsync(&offs, sizeof(int64_t) * (kRadix * nblocks + 1), st);
     const int32_t *kin = keys;
     const int32_t *vin = nullptr;  // pass 0 payload = item index
     for (int pass = 0; pass < passes && !err; ++pass) {
@@ -313,12 +324,9 @@ static cudaError_t radix_sort_index(const int32_t *keys, int64_t count, int key_
         kin = kout;
         vin = vout;
     }
-    cudaFreeAsync(kbuf[0], st);
-    cudaFreeAsync(kbuf[1], st);
-    cudaFreeAsync(vbuf[0], st);
-    cudaFreeAsync(vbuf[1], st);
-    cudaFreeAsync(hist, st);
-    cudaFreeAsync(offs, st);
+    // every buffer allocated so far, also when a later allocation failed
+    for (void *p : {(void *)kbuf[0], (void *)kbuf[1], (void *)vbuf[0], (void *)vbuf[1], (void *)hist, (void *)offs})
+        if (p) cudaFreeAsync(p, st);
     return err;
 }
 
@@ -365,6 +373,13 @@ static cudaError_t merge_path_schedule(int32_t n, int64_t e, const int64_t *row_
     return cudaGetLastError();
 }
 
+// heavy_slot[deg_order[s]] = s for the n_heavy vertices of largest in-degree
+// (deg_order's head: in-degree >= kHeavyInDeg); -1 elsewhere (memset)
+__global__ void k_heavy_slots(int32_t nh, const int32_t *__restrict__ deg_order, int32_t *heavy_slot) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < nh) heavy_slot[deg_order[s]] = s;
+}
+
 __global__ void k_degree_desc_keys(int32_t n, const int32_t *__restrict__ in_deg, int32_t *keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         keys[i] = 0x7FFFFFFF - in_deg[i];
@@ -393,16 +408,16 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     // 1+2. range check and degrees in one pass, max in-degree; read back
     // together (the library's only host sync)
     {
-        unsigned long long *rb_d;  // [first bad edge, max in-degree]
-        SAGA_TRY(cudaMallocAsync(&rb_d, 2 * sizeof(unsigned long long), st));
+        unsigned long long *rb_d;  // [first bad edge, max in-degree, heavy rows]
+        SAGA_TRY(cudaMallocAsync(&rb_d, 3 * sizeof(unsigned long long), st));
         SAGA_TRY(cudaMemsetAsync(rb_d, 0xFF, sizeof(unsigned long long), st));
-        SAGA_TRY(cudaMemsetAsync(rb_d + 1, 0, sizeof(unsigned long long), st));
+        SAGA_TRY(cudaMemsetAsync(rb_d + 1, 0, 2 * sizeof(unsigned long long), st));
         if (e > 0)
             k_range_degrees<<<grid_for(e, 256), 256, 0, st>>>(n, e, src, dst, etype, num_etypes, rb_d, g->in_deg,
                                                               g->out_deg);
         if (n > 0) k_max_deg<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, rb_d + 1);
         SAGA_TRY(cudaGetLastError());
-        unsigned long long rb_h[2] = {0, 0};
+        unsigned long long rb_h[3] = {0, 0, 0};
         SAGA_TRY(cudaMemcpyAsync(rb_h, rb_d, sizeof rb_h, cudaMemcpyDeviceToHost, st));
         SAGA_TRY(cudaStreamSynchronize(st));
         cudaFreeAsync(rb_d, st);
@@ -412,6 +427,7 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
             return SAGA_ERANGE;
         }
         g->max_in_deg = (int32_t)rb_h[1];
+        g->n_heavy = (int32_t)rb_h[2];
     }
 
     // 3. row_ptr
@@ -438,6 +454,13 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
         SAGA_TRY(cudaGetLastError());
         SAGA_TRY(radix_sort_index(keys, n, 31, g->deg_order, st));
         cudaFreeAsync(keys, st);
+    }
+    // heavy rows (in-degree >= kHeavyInDeg): the fp64 ApplyVertex of the gated / GGNN layers
+    SAGA_TRY(cudaMallocAsync(&g->heavy_slot, sizeof(int32_t) * nn, st));
+    SAGA_TRY(cudaMemsetAsync(g->heavy_slot, 0xFF, sizeof(int32_t) * nn, st));
+    if (g->n_heavy > 0) {
+        k_heavy_slots<<<(g->n_heavy + 255) / 256, 256, 0, st>>>(g->n_heavy, g->deg_order, g->heavy_slot);
+        SAGA_TRY(cudaGetLastError());
     }
 
     // 6. merge-path schedules: exactly one task per resident warp (the
@@ -489,7 +512,7 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
 void free_graph(GraphDev *g) {
     cudaStream_t st = g->stream;
     void *ptrs[] = {g->row_ptr,  g->col_src,  g->edge_id,  g->etype,   g->in_deg,  g->out_deg, g->dinv,
-                    g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->trow_ptr, g->tcol_src, g->tinv_deg,
+                    g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->trow_ptr, g->tcol_src, g->tinv_deg,
                     g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, st);

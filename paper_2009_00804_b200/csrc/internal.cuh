@@ -12,6 +12,9 @@
 namespace saga {
 
 constexpr int kNumSMs = 148;
+// Rows whose in-degree reaches this run the gated / GGNN ApplyVertex in fp64
+// (gru_f64.cu): their summed message outgrows the tensor core's fp32 accumulator.
+constexpr int32_t kHeavyInDeg = 256;
 
 // ---- Programmatic dependent launch (PDL) ----------------------------------
 // Inside one saga_layer call every kernel after the first is launched with
@@ -65,8 +68,10 @@ struct GraphDev {
     int32_t *out_deg = nullptr;   // [n]
     float *dinv = nullptr;        // [n]  in_deg^-1/2 (0 if 0)  -- S1, GCN
     float *inv_deg = nullptr;     // [n]  1/in_deg (0 if 0)     -- S1, SAGE
-    int32_t *deg_order = nullptr; // [n]  vertices by in-degree, descending (LSTM work queue)
+    int32_t *deg_order = nullptr; // [n]  vertices by in-degree, descending, ties by id (LSTM work queue)
     int32_t max_in_deg = 0;       // host copy (read back with the range check)
+    int32_t n_heavy = 0;          // host: #vertices with in-degree >= kHeavyInDeg (= the head of deg_order)
+    int32_t *heavy_slot = nullptr; // [n]  v's position in deg_order if v is heavy, else -1
     // Merge-path load-balance schedule (S6): items = E edges + N row ends,
     // task k covers items [k*T, min((k+1)T, E+N)); its start coordinate is
     // (task_v[k], task_p[k]).  Arrays have ntasks+1 entries.
@@ -126,8 +131,9 @@ cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const flo
 // GATED / RGCN typed sums over the typed view (mean = per-type means, R-GCN):
 // S[v][t][:] for t < T (layout [n][T][f], fp32 out, fp64 accumulation); without
 // edge types T = 1 and the plain CSR is used.
-cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, AggWorkspace ws,
-                                 cudaStream_t st);
+// Sx (nullable): the heavy rows' sums also in fp64, [n_heavy][T][f] (gated layer).
+cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, double *Sx,
+                                 AggWorkspace ws, cudaStream_t st);
 
 // ----------------------------------------------------------------- GEMM ----
 enum GemmEpi { EPI_ROWSCALE = 0, EPI_BIAS_ACT = 1, EPI_GAT = 2 };
@@ -147,12 +153,24 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char **why);
 
-// fp32 GEMM + GRU (gemm_f32.cu), config C4.
-cudaError_t launch_gated_apply(int64_t M, int32_t f, int32_t T, const float *S, const float *H, const float *W_type,
-                               const float *W_ih, const float *W_hh, const float *b_ih, const float *b_hh,
-                               float *m_ws, float *out, cudaStream_t st);
+// Heavy rows deg_order[0 .. n_heavy) of the gated / GGNN layers (gru_f64.cu):
+// fp64 ApplyVertex -- the message GEMM from Sx [n_heavy][T][f] (gated) or m
+// from mx [n_heavy][f] (GGNN), then the GRU -- and, for GGNN, the heavy rows'
+// B = H W_b + b_e in fp64 for the edge-MLP gather.  Workspace: HeavyWs.
+struct HeavyWs {
+    double *Sx = nullptr, *Bx = nullptr, *mx = nullptr, *W64 = nullptr;
+    int T = 0;
+};
+size_t heavy_workspace_bytes(const GraphDev &g, saga_model kind, int32_t f);
+HeavyWs heavy_ws(const GraphDev &g, saga_model kind, void *base);
+cudaError_t launch_heavy_weights_f64(const GraphDev &g, const HeavyWs &w, const float *W_type, const float *W_ih,
+                                     const float *W_hh, const float *W_e, cudaStream_t st);
+cudaError_t launch_ggnn_heavy_b(const GraphDev &g, const HeavyWs &w, const float *H, const float *b_e,
+                                cudaStream_t st);
+cudaError_t launch_gru_heavy_f64(const GraphDev &g, const HeavyWs &w, const float *H, const float *b_ih,
+                                 const float *b_hh, float *out, cudaStream_t st);
 
-// split-TF32 (4 MMAs per product) tcgen05 GEMMs (gemm_tf32split.cu), config C4.
+// split-TF32 (3 MMAs per product) tcgen05 GEMMs (gemm_tf32split.cu), config C4.
 // GGNN (NEXT-4): AB = H . [W_a | W_b] + [0 | b_e] (split-TF32, also splits the
 // GRU weights into wsplit), the edge-MLP gather m = sum|max act(A[u] + B[v]),
 // and the GRU GEMM over [m || h].
@@ -168,11 +186,16 @@ cudaError_t launch_sage_fused(const GraphDev &g, const __nv_bfloat16 *X, int32_t
                               cudaStream_t st, const char **why);
 
 size_t ggnn_tc_workspace_floats(int32_t f);
-cudaError_t launch_ggnn_edge_tc(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e,
-                                const float *W_ih, const float *W_hh, float *wsplit, float *AB, cudaStream_t st,
-                                const char **why);
+cudaError_t launch_ggnn_split_weights(int32_t f, const float *W_e, const float *b_e, const float *W_ih,
+                                      const float *W_hh, float *wsplit, cudaStream_t st);
+// GGNN edge-MLP projection AB = H . [W_a | W_b] + [0 | b_e] on the int8 tensor
+// cores with exact accumulation (gemm_i8x.cu); ws: ggnn_i8_workspace_bytes(M).
+size_t ggnn_i8_workspace_bytes(int64_t M);
+cudaError_t launch_ggnn_edge_i8x(int64_t M, int32_t f, const float *H, const float *W_e, const float *b_e, void *ws,
+                                 float *AB, cudaStream_t st, const char **why);
+// Bx: the heavy rows' B = H W_b + b_e in fp64 [n_heavy][f]; mx: their m in fp64 (out).
 cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t f, bool relu, bool max, float *m,
-                                    AggWorkspace ws, cudaStream_t st);
+                                    const double *Bx, double *mx, AggWorkspace ws, cudaStream_t st);
 cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float *H, const float *b_ih,
                                const float *b_hh, const float *wsplit, float *out, cudaStream_t st, const char **why);
 size_t gated_tc_workspace_floats(int32_t f, int32_t T);
@@ -182,10 +205,10 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
                                   const char **why);
 
 // GraphSAGE-LSTM Gather (lstm_gather.cu, NEXT-2): h_out[v] = final LSTM state over v's in-edges.
-size_t lstm_workspace_bytes();  // staged W_hh^T
+size_t lstm_workspace_bytes();  // staged W_hh^T + the work-queue head
 cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const __nv_bfloat16 *W_hh,
-                               const float *b_ih, const float *b_hh, __nv_bfloat16 *h_out, int32_t *queue,
-                               void *wt_ws, cudaStream_t st);
+                               const float *b_ih, const float *b_hh, __nv_bfloat16 *h_out, void *wt_ws,
+                               cudaStream_t st);
 
 // R-GCN ApplyVertex (NEXT-3): out = act([S_0..S_{T-1} || H] . [W_0; ..; W_{T-1}; W_self] + b), 3xTF32.
 size_t rgcn_tc_workspace_floats(int32_t f, int32_t T);

@@ -144,13 +144,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t lstm_workspace_bytes() { return sizeof(uint4) * 4 * kF * kF / 8; }
+// [staged W_hh^T | work-queue head]: the head lives in this region, not among
+// the split-row ticket counters (which every completed call leaves zero); the
+// staging kernel resets it before every gather
+size_t lstm_workspace_bytes() { return sizeof(uint4) * 4 * kF * kF / 8 + 16; }
 
 cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const __nv_bfloat16 *W_hh,
-                               const float *b_ih, const float *b_hh, __nv_bfloat16 *h_out, int32_t *queue,
-                               void *wt_ws, cudaStream_t st) {
+                               const float *b_ih, const float *b_hh, __nv_bfloat16 *h_out, void *wt_ws,
+                               cudaStream_t st) {
     if (g.n == 0) return cudaSuccess;
     uint4 *wt = static_cast<uint4 *>(wt_ws);
+    int32_t *queue = reinterpret_cast<int32_t *>(wt + 4 * kF * kF / 8);
     cudaError_t e = launch(k_stage_whh, (4 * kF * kF / 8 + 255) / 256, 256, 0, st, W_hh, wt, queue);
     if (e) return e;
     int dev = 0, sms = kNumSMs;

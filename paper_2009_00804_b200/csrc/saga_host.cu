@@ -159,7 +159,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Workspace plan: [counters | partials | model intermediates].
 struct Plan {
-    size_t counters = 0, partials = 0, inter0 = 0, inter1 = 0, inter2 = 0, total = 0;
+    size_t counters = 0, partials = 0, inter0 = 0, inter1 = 0, inter2 = 0, inter3 = 0, total = 0;
 };
 
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
@@ -206,15 +206,89 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GGNN:
             p.inter0 = align_up(sizeof(float) * n * 2 * (size_t)std::max(o.in_dim, 0));        // AB = [A | B]
             p.inter1 = align_up(sizeof(float) * n * (size_t)std::max(o.in_dim, 0));            // m
-            p.inter2 = align_up(sizeof(float) * saga::ggnn_tc_workspace_floats(128));           // split W_e, GRU
+            p.inter2 = align_up(sizeof(float) * saga::ggnn_tc_workspace_floats(128)) +         // split GRU weights
+                       align_up(saga::ggnn_i8_workspace_bytes((int64_t)n));                    // int8 digit planes
             break;
         case SAGA_RGCN:
             p.inter0 = align_up(sizeof(float) * n * (size_t)g.num_etypes * (size_t)std::max(o.in_dim, 0));  // S (type means)
             p.inter2 = align_up(sizeof(float) * saga::rgcn_tc_workspace_floats(128, 4));        // split W
             break;
     }
-    p.total = p.counters + p.partials + p.inter0 + p.inter1 + p.inter2;
+    // gated / GGNN heavy rows: the fp64 sums (Sx) or B and m (Bx, mx), gru_f64.cu
+    p.inter3 = align_up(saga::heavy_workspace_bytes(g, kind, std::max(o.in_dim, 0)));
+    p.total = p.counters + p.partials + p.inter0 + p.inter1 + p.inter2 + p.inter3;
     return p;
+}
+
+// Every argument check of saga_layer, before anything is enqueued (saga.h).
+saga_status validate(saga_model kind, const saga::GraphDev &d, const saga_tensor *x, const saga_weights *w,
+                     const saga_layer_opts &o) {
+    switch (kind) {
+        case SAGA_GCN:
+            if (!w->W) return fail(SAGA_EINVAL, "GCN needs W");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GCN act must be NONE/RELU");
+            if (x->dtype == SAGA_F32) {
+                if (!(o.in_dim == 16 || o.in_dim == 32 || o.in_dim == 64 || o.in_dim == 128) || o.out_dim < 1 ||
+                    o.out_dim > 64)
+                    return fail(SAGA_EUNSUPPORTED, "fp32 GCN supports in_dim in {16,32,64,128}, out_dim <= 64");
+                return SAGA_OK;
+            }
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GCN features must be F32 or BF16");
+            if (o.in_dim % 64 || o.in_dim > 256 || o.in_dim == 0 ||
+                !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "bf16 GCN supports in_dim in {64..256 step 64}, out_dim in {64,128,256}");
+            return SAGA_OK;
+        case SAGA_SAGE:
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE supports BF16 features");
+            if (!w->W) return fail(SAGA_EINVAL, "SAGE needs W");
+            if (!(o.in_dim == 64 || o.in_dim == 128) || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "SAGE supports in_dim in {64,128}, out_dim in {64,128,256}");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE act must be NONE/RELU");
+            if (o.fused && !saga::sage_fused_supported(o.in_dim, o.out_dim))
+                return fail(SAGA_EUNSUPPORTED, "fused SAGE supports in_dim 128, out_dim 64 or 128");
+            return SAGA_OK;
+        case SAGA_GAT:
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GAT supports BF16 features");
+            if (!w->W || !w->attn_src || !w->attn_dst) return fail(SAGA_EINVAL, "GAT needs W, attn_src, attn_dst");
+            if (o.heads != 8 || o.head_dim != 8 || o.out_dim != 64 || o.in_dim % 64 || o.in_dim > 256 || !o.in_dim)
+                return fail(SAGA_EUNSUPPORTED, "GAT supports heads=8, head_dim=8, in_dim in {64..256 step 64}");
+            if (o.act != SAGA_ACT_ELU) return fail(SAGA_EUNSUPPORTED, "GAT act must be ELU");
+            if (!(o.leaky_slope >= 0.0f && o.leaky_slope <= 1.0f))
+                return fail(SAGA_EUNSUPPORTED, "GAT leaky_slope must lie in [0, 1]");
+            return SAGA_OK;
+        case SAGA_GATED:
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GATED supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GATED supports in=out=128");
+            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "GATED supports <= 4 edge types");
+            if (!w->W_type || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "GATED needs W_type, W_ih, W_hh, b_ih, b_hh");
+            return SAGA_OK;
+        case SAGA_SAGE_LSTM:
+            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE_LSTM supports BF16 features");
+            if (o.in_dim != 128 || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
+                return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM supports in_dim 128, out_dim in {64,128,256}");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM act must be NONE/RELU");
+            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "SAGE_LSTM needs W, W_ih, W_hh, b_ih, b_hh");
+            return SAGA_OK;
+        case SAGA_GGNN:
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GGNN supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GGNN supports in=out=128");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GGNN act must be NONE/RELU");
+            if (o.aggregator != SAGA_AGG_SUM && o.aggregator != SAGA_AGG_MAX)
+                return fail(SAGA_EUNSUPPORTED, "GGNN aggregator must be SUM or MAX");
+            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
+                return fail(SAGA_EINVAL, "GGNN needs W (edge MLP), W_ih, W_hh, b_ih, b_hh");
+            return SAGA_OK;
+        case SAGA_RGCN:
+            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "RGCN supports F32 features");
+            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "RGCN supports in=out=128");
+            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "RGCN supports <= 4 edge types");
+            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "RGCN act must be NONE/RELU");
+            if (!w->W_type || !w->W) return fail(SAGA_EINVAL, "RGCN needs W_type and W (self)");
+            return SAGA_OK;
+    }
+    return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
 }
 
 }  // namespace
@@ -327,6 +401,8 @@ void saga_free(saga_graph *g) {
     delete g;
 }
 
+
+
 saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *x, const saga_weights *w,
                        saga_tensor *out, const saga_layer_opts *opts, void *workspace, size_t workspace_bytes,
                        void *cuda_stream) {
@@ -336,6 +412,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     const GraphDev &d = g->d;
     const saga_layer_opts &o = *opts;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (kind < SAGA_GCN || kind > SAGA_GGNN) return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
     if (x->rows != d.n) return fail(SAGA_ESHAPE, "features.rows=%lld != N=%d", (long long)x->rows, d.n);
     if (x->cols != o.in_dim) return fail(SAGA_ESHAPE, "features.cols=%lld != in_dim=%d", (long long)x->cols, o.in_dim);
     if (out->rows != d.n || out->cols != o.out_dim)
@@ -348,6 +425,8 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     const Plan plan = plan_for(kind, d, o);
     if (workspace_bytes < plan.total || (plan.total && !workspace))
         return fail(SAGA_EINVAL, "workspace too small: %zu < %zu", workspace_bytes, plan.total);
+    const saga_status vs = validate(kind, d, x, w, o);
+    if (vs != SAGA_OK) return vs;
     if (d.n == 0) return SAGA_OK;
 
     uint8_t *ws = static_cast<uint8_t *>(workspace);
@@ -357,38 +436,29 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     uint8_t *i0 = ws + plan.counters + plan.partials;
     uint8_t *i1 = i0 + plan.inter0;
     uint8_t *i2 = i1 + plan.inter1;
+    uint8_t *i3 = i2 + plan.inter2;
     cudaError_t e = cudaSuccess;
     PdlCall pdl_call;
     // split-row tickets start at 0; every ticket's winner resets its counter,
     // so a completed call leaves them zero (opts.workspace_zeroed skips this)
     if (!o.workspace_zeroed && !(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {
-        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * ((size_t)std::max({d.ntasks, d.tntasks, d.fntasks}) + 1),
-                            st);
+        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks}), st);
         if (e) return cuda_fail(e, "memset counters");
     }
     const char *why = "";
 
     switch (kind) {
         case SAGA_GCN: {
-            if (!w->W) return fail(SAGA_EINVAL, "GCN needs W");
-            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GCN act must be NONE/RELU");
             if (x->dtype == SAGA_F32) {
-                if (!(o.in_dim == 16 || o.in_dim == 32 || o.in_dim == 64 || o.in_dim == 128) || o.out_dim < 1 ||
-                    o.out_dim > 64)
-                    return fail(SAGA_EUNSUPPORTED, "fp32 GCN supports in_dim in {16,32,64,128}, out_dim <= 64");
                 {
-                ProfScope ps_("gcn_f32_fused", st);
-                e = launch_gcn_f32_fused(d, static_cast<const float *>(x->data), o.in_dim,
-                                         static_cast<const float *>(w->W), o.out_dim, w->bias, o.act,
-                                         static_cast<float *>(out->data), aw, st);
-            }
+                    ProfScope ps_("gcn_f32_fused", st);
+                    e = launch_gcn_f32_fused(d, static_cast<const float *>(x->data), o.in_dim,
+                                             static_cast<const float *>(w->W), o.out_dim, w->bias, o.act,
+                                             static_cast<float *>(out->data), aw, st);
+                }
                 if (e) return cuda_fail(e, "gcn_f32_fused");
                 return SAGA_OK;
             }
-            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GCN features must be F32 or BF16");
-            if (o.in_dim % 64 || o.in_dim > 256 || o.in_dim == 0 ||
-                !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
-                return fail(SAGA_EUNSUPPORTED, "bf16 GCN supports in_dim in {64..256 step 64}, out_dim in {64,128,256}");
             // S2: Y = diag(dinv) . X . W  (tcgen05), then S3-S5 aggregation
             __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(i0);
             GemmArgs a;
@@ -411,13 +481,6 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             return SAGA_OK;
         }
         case SAGA_SAGE: {
-            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE supports BF16 features");
-            if (!w->W) return fail(SAGA_EINVAL, "SAGE needs W");
-            if (!(o.in_dim == 64 || o.in_dim == 128) || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
-                return fail(SAGA_EUNSUPPORTED, "SAGE supports in_dim in {64,128}, out_dim in {64,128,256}");
-            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE act must be NONE/RELU");
-            if (o.fused && !sage_fused_supported(o.in_dim, o.out_dim))
-                return fail(SAGA_EUNSUPPORTED, "fused SAGE supports in_dim 128, out_dim 64 or 128");
             if (o.fused) {
                 // NEXT-1: mean aggregation and the concat-GEMM in one kernel
                 {
@@ -452,13 +515,6 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             return SAGA_OK;
         }
         case SAGA_GAT: {
-            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "GAT supports BF16 features");
-            if (!w->W || !w->attn_src || !w->attn_dst) return fail(SAGA_EINVAL, "GAT needs W, attn_src, attn_dst");
-            if (o.heads != 8 || o.head_dim != 8 || o.out_dim != 64 || o.in_dim % 64 || o.in_dim > 256 || !o.in_dim)
-                return fail(SAGA_EUNSUPPORTED, "GAT supports heads=8, head_dim=8, in_dim in {64..256 step 64}");
-            if (o.act != SAGA_ACT_ELU) return fail(SAGA_EUNSUPPORTED, "GAT act must be ELU");
-            if (!(o.leaky_slope >= 0.0f && o.leaky_slope <= 1.0f))
-                return fail(SAGA_EUNSUPPORTED, "GAT leaky_slope must lie in [0, 1]");
             __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(i0);
             float *el = reinterpret_cast<float *>(i1), *er = reinterpret_cast<float *>(i2);
             GemmArgs a;
@@ -481,42 +537,32 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             return SAGA_OK;
         }
         case SAGA_GATED: {
-            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GATED supports F32 features");
-            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GATED supports in=out=128");
-            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "GATED supports <= 4 edge types");
-            if (!w->W_type || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
-                return fail(SAGA_EINVAL, "GATED needs W_type, W_ih, W_hh, b_ih, b_hh");
             float *S = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
+            const float *H = static_cast<const float *>(x->data);
+            const HeavyWs hw = heavy_ws(d, SAGA_GATED, i3);
             {
                 ProfScope ps_("agg_typed_f32", st);
-                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, false, aw, st);
+                e = launch_agg_typed_f32(d, H, o.in_dim, S, false, hw.Sx, aw, st);
             }
             if (e) return cuda_fail(e, "typed aggregate");
-            if (getenv("SAGA_GATED_SIMT")) {  // development knob: the FFMA reference kernels
-                ProfScope ps_("gated_apply_sgemm", st);
-                e = launch_gated_apply(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data), w->W_type,
-                                       static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
-                                       w->b_ih, w->b_hh, m, static_cast<float *>(out->data), st);
-                if (e) return cuda_fail(e, "gated apply");
-                return SAGA_OK;
-            }
             {
                 ProfScope ps_("gated_apply_tf32x3", st);
-                e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, static_cast<const float *>(x->data),
-                                          w->W_type, static_cast<const float *>(w->W_ih),
-                                          static_cast<const float *>(w->W_hh), w->b_ih, w->b_hh, m,
-                                          reinterpret_cast<float *>(i2), static_cast<float *>(out->data), st, &why);
+                e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, H, w->W_type,
+                                          static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
+                                          w->b_ih, w->b_hh, m, reinterpret_cast<float *>(i2),
+                                          static_cast<float *>(out->data), st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "gated apply: %s (%s)", cudaGetErrorString(e), why);
+            if (d.n_heavy) {
+                ProfScope ps_("gru_heavy_f64", st);
+                e = launch_heavy_weights_f64(d, hw, w->W_type, static_cast<const float *>(w->W_ih),
+                                             static_cast<const float *>(w->W_hh), nullptr, st);
+                if (!e) e = launch_gru_heavy_f64(d, hw, H, w->b_ih, w->b_hh, static_cast<float *>(out->data), st);
+            }
+            if (e) return cuda_fail(e, "gated heavy rows");
             return SAGA_OK;
         }
         case SAGA_SAGE_LSTM: {
-            if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE_LSTM supports BF16 features");
-            if (o.in_dim != 128 || !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
-                return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM supports in_dim 128, out_dim in {64,128,256}");
-            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "SAGE_LSTM act must be NONE/RELU");
-            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
-                return fail(SAGA_EINVAL, "SAGE_LSTM needs W, W_ih, W_hh, b_ih, b_hh");
             const int F = o.in_dim;
             __nv_bfloat16 *P = reinterpret_cast<__nv_bfloat16 *>(i0);
             __nv_bfloat16 *hagg = reinterpret_cast<__nv_bfloat16 *>(i1);
@@ -536,9 +582,8 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (e) return fail(SAGA_ECUDA, "lstm input gemm: %s (%s)", cudaGetErrorString(e), why);
             {
                 ProfScope ps_("lstm_gather", st);
-                // the work-queue head lives in the counters' spare last slot (never a ticket)
-                e = launch_lstm_gather(d, P, static_cast<const __nv_bfloat16 *>(w->W_hh), w->b_ih, w->b_hh, hagg,
-                                       aw.counters + std::max({d.ntasks, d.tntasks, d.fntasks}), i2, st);
+                e = launch_lstm_gather(d, P, static_cast<const __nv_bfloat16 *>(w->W_hh), w->b_ih, w->b_hh, hagg, i2,
+                                       st);
             }
             if (e) return cuda_fail(e, "lstm gather");
             GemmArgs a;
@@ -558,27 +603,37 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             return SAGA_OK;
         }
         case SAGA_GGNN: {
-            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GGNN supports F32 features");
-            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "GGNN supports in=out=128");
-            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "GGNN act must be NONE/RELU");
-            if (o.aggregator != SAGA_AGG_SUM && o.aggregator != SAGA_AGG_MAX)
-                return fail(SAGA_EUNSUPPORTED, "GGNN aggregator must be SUM or MAX");
-            if (!w->W || !w->W_ih || !w->W_hh || !w->b_ih || !w->b_hh)
-                return fail(SAGA_EINVAL, "GGNN needs W (edge MLP), W_ih, W_hh, b_ih, b_hh");
             const float *H = static_cast<const float *>(x->data);
             float *AB = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
             float *wsplit = reinterpret_cast<float *>(i2);
             {
-                ProfScope ps_("ggnn_edge_tf32x3", st);
-                e = launch_ggnn_edge_tc(d.n, o.in_dim, H, static_cast<const float *>(w->W), w->bias,
-                                        static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
-                                        wsplit, AB, st, &why);
+                ProfScope ps_("ggnn_split_weights", st);
+                e = launch_ggnn_split_weights(o.in_dim, static_cast<const float *>(w->W), w->bias,
+                                              static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
+                                              wsplit, st);
+            }
+            if (e) return cuda_fail(e, "ggnn split weights");
+            {
+                // edge-MLP projection on the int8 tensor cores, exact accumulation (unbiased A, B)
+                ProfScope ps_("ggnn_edge_i8x", st);
+                e = launch_ggnn_edge_i8x(d.n, o.in_dim, H, static_cast<const float *>(w->W), w->bias,
+                                         reinterpret_cast<uint8_t *>(wsplit) +
+                                             align_up(sizeof(float) * ggnn_tc_workspace_floats(128)),
+                                         AB, st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "ggnn edge gemm: %s (%s)", cudaGetErrorString(e), why);
+            const HeavyWs hw = heavy_ws(d, SAGA_GGNN, i3);
+            if (d.n_heavy) {
+                ProfScope ps_("ggnn_heavy_b_f64", st);
+                e = launch_heavy_weights_f64(d, hw, nullptr, static_cast<const float *>(w->W_ih),
+                                             static_cast<const float *>(w->W_hh), static_cast<const float *>(w->W), st);
+                if (!e) e = launch_ggnn_heavy_b(d, hw, H, w->bias, st);
+            }
+            if (e) return cuda_fail(e, "ggnn heavy B");
             {
                 ProfScope ps_("agg_edge_mlp_f32", st);
                 e = launch_agg_edge_mlp_f32(d, AB, o.in_dim, o.act == SAGA_ACT_RELU, o.aggregator == SAGA_AGG_MAX, m,
-                                            aw, st);
+                                            hw.Bx, hw.mx, aw, st);
             }
             if (e) return cuda_fail(e, "ggnn edge-mlp gather");
             {
@@ -587,18 +642,18 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                                        st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "ggnn gru: %s (%s)", cudaGetErrorString(e), why);
+            if (d.n_heavy) {
+                ProfScope ps_("gru_heavy_f64", st);
+                e = launch_gru_heavy_f64(d, hw, H, w->b_ih, w->b_hh, static_cast<float *>(out->data), st);
+            }
+            if (e) return cuda_fail(e, "ggnn heavy rows");
             return SAGA_OK;
         }
         case SAGA_RGCN: {
-            if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "RGCN supports F32 features");
-            if (o.in_dim != 128 || o.out_dim != 128) return fail(SAGA_EUNSUPPORTED, "RGCN supports in=out=128");
-            if (d.num_etypes > 4) return fail(SAGA_EUNSUPPORTED, "RGCN supports <= 4 edge types");
-            if (o.act != SAGA_ACT_NONE && o.act != SAGA_ACT_RELU) return fail(SAGA_EUNSUPPORTED, "RGCN act must be NONE/RELU");
-            if (!w->W_type || !w->W) return fail(SAGA_EINVAL, "RGCN needs W_type and W (self)");
             float *S = reinterpret_cast<float *>(i0);
             {
                 ProfScope ps_("agg_typed_mean_f32", st);
-                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, true, aw, st);
+                e = launch_agg_typed_f32(d, static_cast<const float *>(x->data), o.in_dim, S, true, nullptr, aw, st);
             }
             if (e) return cuda_fail(e, "rgcn typed aggregate");
             {
@@ -611,7 +666,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             return SAGA_OK;
         }
     }
-    return fail(SAGA_EINVAL, "unknown model kind %d", (int)kind);
+    return fail(SAGA_EINTERNAL, "unreachable model kind %d", (int)kind);
 }
 
 }  // extern "C"

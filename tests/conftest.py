@@ -25,3 +25,30 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _parity_test_id(request):
+    """Tags tests.harness.check() records with the running test's id."""
+    try:
+        from tests import harness
+    except Exception:  # pragma: no cover
+        yield
+        return
+    harness.CURRENT_TEST[0] = request.node.nodeid
+    yield
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With SAGA_PARITY_LOG set, write every parity check's normwise and
+    per-row error to that file as JSON."""
+    path = os.environ.get("SAGA_PARITY_LOG")
+    if not path:
+        return
+    try:
+        from tests import harness
+    except Exception:  # pragma: no cover
+        return
+    import json
+    with open(path, "w") as f:
+        json.dump(harness.RECORDS, f, indent=0)

@@ -11,6 +11,30 @@ import torch
 import workloads as W
 
 TOL = {"f32": 1e-4, "bf16": 2e-2}   # BASELINE.json north_star, normwise inf-relative (A18)
+# SURVEY.md 8(c)'s per-row diagnostic ||y_v - yref_v|| / max(||yref_v||, 1e-3 ||yref||)
+# is reported for every parity check and gated at ROW_GATE x the normwise bar
+ROW_GATE = 10.0
+
+# Every check() of the session: (test id, label, normwise err, per-row err, worst row, tol).
+# tests/conftest.py writes them to $SAGA_PARITY_LOG (JSON) at the end of the session.
+RECORDS: list = []
+CURRENT_TEST = [""]
+
+
+def check(y, ref, tol, label=""):
+    """Parity gate: normwise inf-relative error <= tol (reading A18) and the
+    per-row diagnostic <= ROW_GATE * tol.  Returns (normwise, per-row).
+    (oracle is imported here, not at module level: bench.py's timed path uses
+    this module's gpu_step and must not load the oracle.)"""
+    import oracle
+    yy = to_np(y) if isinstance(y, torch.Tensor) else np.asarray(y, dtype=np.float64)
+    err = oracle.rel_err(yy, ref)
+    rerr, row = oracle.row_err(yy, ref)
+    RECORDS.append({"test": CURRENT_TEST[0], "label": label, "err": err, "row_err": rerr, "worst_row": row,
+                    "tol": tol})
+    assert err <= tol, f"{label}: normwise rel err {err:.3e} > {tol}"
+    assert rerr <= ROW_GATE * tol, f"{label}: per-row err {rerr:.3e} (row {row}) > {ROW_GATE} x {tol}"
+    return err, rerr
 
 
 def dev_inputs(d, dev):

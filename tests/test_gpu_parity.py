@@ -147,9 +147,8 @@ def test_layer_zoo(saga, model, name, n, s, d, loops):
     og = H.oracle_graph(oracle, cfg, x)
     refs = H.oracle_step(oracle, cfg, og, x, layer_inputs=[None, outs[0].cpu()] if model == "sage" else None)
     tol = H.TOL[cfg.dtype]
-    for y, ref in zip(outs, refs):
-        err = oracle.rel_err(H.to_np(y), ref)
-        assert err <= tol, f"{model}/{name}: rel err {err:.3e} > {tol}"
+    for i, (y, ref) in enumerate(zip(outs, refs)):
+        H.check(y, ref, tol, f"{model}/{name}/loops={loops}/layer{i}")
 
 
 # ----------------------------------------------------- configured steps ----
@@ -167,14 +166,13 @@ def _config_check(saga, cfg, rows_k=None):
     tol = H.TOL[cfg.dtype]
     li = [None, outs[0].cpu()] if cfg.model == "sage" else None
     refs = H.oracle_step(oracle, cfg, og, d, rows=rows, layer_inputs=li)
-    for y, ref in zip(outs, refs):
+    for i, (y, ref) in enumerate(zip(outs, refs)):
         yy = H.to_np(y if rows is None else y[torch.from_numpy(rows).to(y.device)])
-        err = oracle.rel_err(yy, ref)
-        assert err <= tol, f"{cfg.name}: rel err {err:.3e} > {tol}"
+        H.check(yy, ref, tol, f"{cfg.name}/layer{i}")
     if cfg.model == "sage":   # end to end: the oracle chains its own fp64 H1 (A19)
         ref_e2e = H.oracle_step(oracle, cfg, og, d, rows=rows)[1]
         yy = H.to_np(outs[1] if rows is None else outs[1][torch.from_numpy(rows).to(DEV)])
-        assert oracle.rel_err(yy, ref_e2e) <= tol
+        H.check(yy, ref_e2e, tol, f"{cfg.name}/end-to-end")
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C8"])
@@ -250,41 +248,63 @@ def test_typed_view(saga, model, T, types):
     torch.cuda.synchronize()
     og = H.oracle_graph(oracle, cfg, x)
     refs = H.oracle_step(oracle, cfg, og, x)
-    err = oracle.rel_err(H.to_np(outs[0]), refs[0])
-    assert err <= H.TOL["f32"], f"{model} T={T} {types}: rel err {err:.3e}"
+    H.check(outs[0], refs[0], H.TOL["f32"], f"{model} T={T} {types}")
 
 
+@pytest.mark.parametrize("hub", [1500, 6000, 20000])
 @pytest.mark.parametrize("agg", ["sum", "max"])
 @pytest.mark.parametrize("relu", [True, False])
-def test_ggnn_aggregators(saga, agg, relu):
+def test_ggnn_aggregators(saga, agg, relu, hub):
     """NEXT-4 paper-form GGNN: both Gather reductions, with and without the
-    edge-MLP ReLU, on a power-law graph with a hub split across tasks.
-
-    Conditioning: with ReLU and sum the hub's message m grows linearly with
-    its in-degree (all terms >= 0), and the fp32 rounding of m alone moves
-    the GRU output by ~u_fp32 |m| |W_ih| sqrt(f): 1.2e-4 normwise at
-    in-degree 6000 here, past the 1e-4 fp32 bar; the hub is kept at 1500."""
+    edge-MLP ReLU, on a power-law graph (zipf in-degrees: vertex 0 already
+    receives ~14K edges) with one more hub of `hub` in-edges, split across
+    tasks.  With ReLU and sum the hubs' messages grow linearly with their
+    in-degree (every term >= 0; |m| ~ 1.5e4 at 6K in-edges): rows with
+    in-degree >= 256 run ApplyVertex in fp64 (gru_f64.cu), whose error is set
+    by the fp32 storage of m (~4e-6); the split-TF32 tensor-core GEMM
+    (fp32 accumulator) misses the fp32 bar on such rows (1.35e-4 at 6K,
+    scripts/tc_accum_probe.py)."""
     n = 2500
     rng = np.random.default_rng(7)
     s = rng.integers(0, n, 30000).astype(np.int32)
     d = np.minimum(rng.zipf(1.7, 30000) - 1, n - 1).astype(np.int32)
-    d[:1500] = 11
+    d[:hub] = 11
     x = _zoo_inputs("ggnn", n, s, d, 3)
     dx = H.dev_inputs(dict(x, src=torch.from_numpy(s), dst=torch.from_numpy(d)), DEV)
     g = saga.saga_graph_build(n, dx["src"], dx["dst"])
     lay = saga.Layer("ggnn", g, 128, 128, saga.SAGA_ACT_RELU if relu else saga.SAGA_ACT_NONE, torch.float32,
                      aggregator=agg)
-    y = lay(dx["H"], {"W": dx["W_e"], "bias": dx["b_e"], "W_ih": dx["W_ih"], "W_hh": dx["W_hh"],
-                      "b_ih": dx["b_ih"], "b_hh": dx["b_hh"]})
-    y2 = lay(dx["H"], {"W": dx["W_e"], "bias": dx["b_e"], "W_ih": dx["W_ih"], "W_hh": dx["W_hh"],
-                       "b_ih": dx["b_ih"], "b_hh": dx["b_hh"]})
+    w = {"W": dx["W_e"], "bias": dx["b_e"], "W_ih": dx["W_ih"], "W_hh": dx["W_hh"], "b_ih": dx["b_ih"],
+         "b_hh": dx["b_hh"]}
+    y = lay(dx["H"], w)
+    y2 = lay(dx["H"], w)
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
     og = oracle.csr_build(n, s, d)
     ref = oracle.ggnn(og, x["H"], x["W_e"], x["b_e"], x["W_ih"], x["W_hh"], x["b_ih"], x["b_hh"],
                       act=1 if relu else 0, agg=agg)
-    err = oracle.rel_err(y.cpu().numpy(), ref)
-    assert err <= H.TOL["f32"], f"ggnn {agg} relu={relu}: rel err {err:.3e}"
+    err, _ = H.check(y, ref, H.TOL["f32"], f"ggnn {agg} relu={relu} hub={hub}")
+    # heavy rows (fp64 ApplyVertex) are as accurate as fp32 storage of m allows
+    assert err <= 2e-5, f"ggnn {agg} relu={relu} hub={hub}: {err:.3e} above the fp64-path level"
+
+
+def test_gated_hub70k_fp64_level(saga):
+    """The gated layer's worst zoo case (a 70K-in-edge hub whose per-type sums
+    reach |S| ~ 130): the hub runs ApplyVertex in fp64, so the layer error is
+    below the fp32 FFMA level measured in round 1 (2.0e-5)."""
+    name, n, s, d = [z for z in zoo.zoo(include_big=True) if z[0] == "hub70k"][0]
+    cfg = _zoo_cfg("gated", n, s.shape[0])
+    x = _zoo_inputs("gated", n, s, d, 7)
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    x["etype"] = torch.from_numpy((np.arange(s.shape[0]) * 7 % 4).astype(np.int32))
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, _ = H.gpu_step(saga, cfg, g, dx)
+    torch.cuda.synchronize()
+    og = H.oracle_graph(oracle, cfg, x)
+    ref = H.oracle_step(oracle, cfg, og, x)[0]
+    err, _ = H.check(outs[0], ref, H.TOL["f32"], "gated hub70k")
+    assert err <= 2e-5, f"gated hub70k: {err:.3e}"
 
 
 def _fused(cfg, n=None, m=None, name=None):
@@ -314,9 +334,8 @@ def test_sage_fused_zoo(saga, name, n, s, d):
     torch.cuda.synchronize()
     og = H.oracle_graph(oracle, cfg, x)
     refs = H.oracle_step(oracle, cfg, og, x, layer_inputs=[None, outs[0].cpu()])
-    for y, ref in zip(outs, refs):
-        err = oracle.rel_err(H.to_np(y), ref)
-        assert err <= H.TOL["bf16"], f"fused sage/{name}: rel err {err:.3e}"
+    for i, (y, ref) in enumerate(zip(outs, refs)):
+        H.check(y, ref, H.TOL["bf16"], f"fused sage/{name}/layer{i}")
 
 
 def _random_graph(seed):
@@ -364,9 +383,8 @@ def test_random_graphs(saga, model, seed):
     og = H.oracle_graph(oracle, cfg, x)
     refs = H.oracle_step(oracle, cfg, og, x, layer_inputs=[None, outs[0].cpu()] if model == "sage" else None)
     tol = H.TOL[cfg.dtype]
-    for y, ref in zip(outs, refs):
-        err = oracle.rel_err(H.to_np(y), ref)
-        assert err <= tol, f"{model}/seed {seed} (n={n}, e={s.shape[0]}): rel err {err:.3e}"
+    for i, (y, ref) in enumerate(zip(outs, refs)):
+        H.check(y, ref, tol, f"{model}/seed {seed} (n={n}, e={s.shape[0]})/layer{i}")
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C8"])
@@ -451,3 +469,42 @@ def test_workspace_zeroed_contract(saga, cfg):
     torch.cuda.synchronize()
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("model", MODELS)
+def test_workspace_reuse_across_graphs(saga, model):
+    """saga.h: every completed call leaves the workspace's ticket counters
+    zero, so a workspace may be reused with workspace_zeroed = 1 for ANOTHER
+    graph with more tasks (round-1 advisor: the LSTM queue head used to sit
+    in a counter slot that a larger graph uses as a ticket)."""
+    n = 3000
+    rng = np.random.default_rng(21)
+    small_s, small_d = rng.integers(0, n, 40).astype(np.int32), rng.integers(0, n, 40).astype(np.int32)
+    big_s = rng.integers(0, n, 60000).astype(np.int32)
+    big_d = np.minimum(rng.zipf(1.6, 60000) - 1, n - 1).astype(np.int32)
+    cfg = _zoo_cfg(model, n, big_s.shape[0])
+    x = _zoo_inputs(model, n, big_s, big_d, 5)
+    et = lambda e: torch.from_numpy((np.arange(e) % 4).astype(np.int32)).to(DEV)
+    typed = model in ("gated", "rgcn")
+    gs = saga.saga_graph_build(n, torch.from_numpy(small_s).to(DEV), torch.from_numpy(small_d).to(DEV),
+                               et(40) if typed else None, 4 if typed else 1)
+    gb = saga.saga_graph_build(n, torch.from_numpy(big_s).to(DEV), torch.from_numpy(big_d).to(DEV),
+                               et(60000) if typed else None, 4 if typed else 1)
+    dx = H.dev_inputs(dict(x, src=torch.from_numpy(big_s), dst=torch.from_numpy(big_d)), DEV)
+    if typed:
+        dx["etype"] = et(60000)
+    fresh, layers = H.gpu_step(saga, cfg, gb, dx)                 # reference: own zero-filled workspace
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in fresh]
+    ws = torch.zeros(max(l.workspace.numel() for l in layers), dtype=torch.uint8, device=DEV)
+    small_layers = H.gpu_step(saga, cfg, gs, dx)[1]
+    for lay_s, lay_b in zip(small_layers, layers):
+        lay_s.workspace, lay_b.workspace = ws, ws
+    H.gpu_step(saga, cfg, gs, dx, small_layers)                   # small graph on the shared workspace
+    for o in fresh:
+        o.zero_()
+    H.gpu_step(saga, cfg, gb, dx, layers, fresh)                  # then the big graph, workspace_zeroed = 1
+    torch.cuda.synchronize()
+    for a, b in zip(fresh, ref):
+        assert torch.equal(a, b)
+    assert int(ws[:64].count_nonzero()) == 0 or model in ("gcn_f32",)  # first ticket counters left zero
