@@ -57,19 +57,31 @@ struct GraphView {
     int64_t T, ntasks;
     int32_t n;
     int32_t e;
+    const int32_t *rmap;  // view row -> output row (nullptr: identity)
 };
 
 GraphView view(const GraphDev &g) {
-    return GraphView{g.row_ptr, g.col_src, g.task_v, g.task_p, g.task_items, g.ntasks, g.n, (int32_t)g.e};
+    return GraphView{g.row_ptr, g.col_src, g.task_v, g.task_p, g.task_items, g.ntasks, g.n, (int32_t)g.e, nullptr};
 }
 // the same CSR with the 4x finer schedule (GAT)
 GraphView view_fine(const GraphDev &g) {
-    return GraphView{g.row_ptr, g.col_src, g.ftask_v, g.ftask_p, g.ftask_items, g.fntasks, g.n, (int32_t)g.e};
+    return GraphView{g.row_ptr, g.col_src, g.ftask_v, g.ftask_p, g.ftask_items, g.fntasks, g.n, (int32_t)g.e,
+                     nullptr};
 }
 // rows (v, t) -> r = v * num_etypes + t (built when the graph has edge types)
 GraphView view_typed(const GraphDev &g) {
     return GraphView{g.trow_ptr, g.tcol_src, g.ttask_v, g.ttask_p, g.ttask_items, g.tntasks,
-                     g.n * g.num_etypes, (int32_t)g.e};
+                     g.n * g.num_etypes, (int32_t)g.e, nullptr};
+}
+// the aggregation rows only (graph_build.cu step 8): rows whose in-edges are
+// nothing but one self-loop, or none, are finished by the GEMM epilogue
+GraphView view_agg(const GraphDev &g) {
+    return GraphView{g.arow_ptr, g.acol_src, g.atask_v, g.atask_p, g.atask_items, g.antasks, g.an, (int32_t)g.ae,
+                     g.arow};
+}
+GraphView view_agg_fine(const GraphDev &g) {
+    return GraphView{g.arow_ptr, g.acol_src, g.aftask_v, g.aftask_p, g.aftask_items, g.afntasks, g.an, (int32_t)g.ae,
+                     g.arow};
 }
 
 __device__ __forceinline__ float act_fn(float x, int act) {
@@ -254,6 +266,7 @@ struct GcnF32FusedOp {
 // online-softmax update: with d = s - m, e = exp(-|d|); if d > 0 the state is
 // rescaled by e and the new term weighs 1, else the new term weighs e.
 // Flush: ELU(acc / l).  Row value: er[v, h] (kWin = 8 heads).
+template <bool kMap>
 struct GatOp {
     static constexpr int kWin = 8;
     static constexpr int kSlot = 128;
@@ -264,7 +277,11 @@ struct GatOp {
     const float *el, *er;
     float slope;
     __nv_bfloat16 *out;
-    __device__ __forceinline__ float row_value(int32_t v, int j) const { return __ldg(er + (int64_t)v * 8 + j); }
+    const int32_t *rmap;  // kMap: the aggregation view's row -> vertex
+    __device__ __forceinline__ float row_value(int32_t v, int j) const {
+        const int32_t u = kMap ? __ldg(rmap + v) : v;
+        return __ldg(er + (int64_t)u * 8 + j);
+    }
     __device__ __forceinline__ void zero(Acc &c) const { c.m = -INFINITY; c.l = 0.f; c.a0 = 0.f; c.a1 = 0.f; }
     __device__ __forceinline__ Val load(int32_t u, int lane) const {
         Val v;
@@ -636,7 +653,7 @@ __device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, 
 // main loop (never inside it), so the hot loop carries no call.
 template <typename Op>
 __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t T, int32_t r, int64_t rb,
-                                          int64_t re, const float *Ws) {
+                                          int64_t re, const float *Ws, const int32_t *rmap) {
     const int lane = threadIdx.x & 31;
     const int64_t k1 = (rb + r) / T, k2 = (re + r) / T;
     // release the partial stores before the ticket; acquire the others'
@@ -656,7 +673,7 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
         op.merge(m, ws.partials + (2 * k1 + 1) * Op::kSlot, lane);
         for (int64_t kk = k1 + 1; kk <= k2; ++kk) op.merge(m, ws.partials + (2 * kk) * Op::kSlot, lane);
         const float rs = Op::kWin ? op.row_value(r, Op::win_col(lane)) : 0.0f;
-        do_finish(op, r, m, rs, lane, Ws, 0);
+        do_finish(op, rmap ? __ldg(rmap + r) : r, m, rs, lane, Ws, 0);
     }
 }
 
@@ -685,15 +702,18 @@ template <typename Op>
 struct has_split_batch<Op, decltype(void(Op::kSplitBatch))> { static constexpr bool value = Op::kSplitBatch; };
 
 // ================================================================== engine ==
-template <int U, typename Val, int kWinD>
+template <int U, typename Val, int kWinD, bool kRmap>
 struct DenseWarp {
     Val park[U][32];
-    int32_t re[32];        // row_end of rows wr .. wr+31
-    float rv[32 * kWinD];  // per-row values of the same rows (kWinD per row)
+    int32_t re[32];                 // row_end of rows wr .. wr+31
+    int32_t rid[kRmap ? 32 : 1];    // their output rows (the view's rmap)
+    float rv[32 * kWinD];           // per-row values of the same rows (kWinD per row)
     int32_t wr, head_end;
 };
 
-template <int U, int kMinB, typename Op>
+// kRmap: the view maps its rows to output rows (the aggregation view); a
+// compile-time switch -- as a runtime one it cost the GAT kernel 25%.
+template <int U, int kMinB, typename Op, bool kRmap>
 __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, const Op op, const AggWorkspace ws,
                                                           const float *Wg, const int32_t w_elems) {
     constexpr int kWin = Op::kWin;
@@ -705,7 +725,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     constexpr bool kSplitBatch = has_split_batch<Op>::value;
     constexpr bool kGroup = has_group_scores<Op>::value;
     static_assert(!(kSplitBatch && kGroup), "grouped-score ops park split batches");
-    using DW = DenseWarp<U, typename Op::Val, kWinD>;
+    using DW = DenseWarp<U, typename Op::Val, kWinD, kRmap>;
     __shared__ DW warps[kWarpsPerBlock];
     extern __shared__ float Ws[];  // epilogue operand staged per block: fused-GEMV weight, or bias
     griddep_launch();
@@ -728,6 +748,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     auto fill_window = [&](int32_t wbase) {
         const int32_t r = wbase + lane;
         VW.re[lane] = r < g.n ? (int32_t)__ldg(g.row_ptr + r + 1) : g.e;
+        if constexpr (kRmap) VW.rid[lane] = r < g.n ? __ldg(g.rmap + r) : 0;
         if (kWin) {
 #pragma unroll
             for (int j = 0; j < kWinD; ++j) {  // value (i % kWinD) of row wbase + i / kWinD
@@ -769,7 +790,10 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
             if (lane == 0) VW.head_end = row_end;
             head_open = false;
         } else {
-            do_finish(op, v, acc, rs, lane, Ws, 0);
+            if constexpr (kRmap)
+                do_finish(op, VW.rid[v - VW.wr], acc, rs, lane, Ws, 0);
+            else
+                do_finish(op, v, acc, rs, lane, Ws, 0);
         }
         ++v;
         if (v - VW.wr == 32) {
@@ -868,11 +892,11 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     if (v < g.n && p1 > row_beg) {  // tail: row v continues into the next task
         const int64_t slot = (head && v == v0) ? 2 * k : 2 * k + 1;
         op.save(ws.partials + slot * Op::kSlot, acc, lane);
-        ticket_merge(op, ws, g.T, v, row_beg, row_end, Ws);
+        ticket_merge(op, ws, g.T, v, row_beg, row_end, Ws, kRmap ? g.rmap : nullptr);
     }
     const int32_t head_end = VW.head_end;
     if (head_end >= 0 && v != v0)  // the head row ended inside this task
-        ticket_merge(op, ws, g.T, v0, head_beg, head_end, Ws);
+        ticket_merge(op, ws, g.T, v0, head_beg, head_end, Ws, kRmap ? g.rmap : nullptr);
 }
 
 template <int U, int kMinB, typename Op>
@@ -881,7 +905,8 @@ cudaError_t run(const GraphView &g, const Op &op, AggWorkspace ws, cudaStream_t 
     if (g.ntasks == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((g.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const size_t smem = Wg ? sizeof(float) * w_elems : 0;
-    return launch(k_segreduce<U, kMinB, Op>, blocks, kBlock, smem, st, g, op, ws, Wg, w_elems);
+    if (g.rmap) return launch(k_segreduce<U, kMinB, Op, true>, blocks, kBlock, smem, st, g, op, ws, Wg, w_elems);
+    return launch(k_segreduce<U, kMinB, Op, false>, blocks, kBlock, smem, st, g, op, ws, Wg, w_elems);
 }
 
 // Small-degree graphs (every in-degree <= kRowwiseMaxDeg): one warp per row,
@@ -930,20 +955,20 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
 }
 
 template <int kAct>
-cudaError_t agg_sum_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, const float *scale,
+cudaError_t agg_sum_bf16(const GraphView &gv, const __nv_bfloat16 *X, int32_t f, const float *scale,
                          const float *bias, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
     switch (f) {
         case 256: {
             SumBf16Op<kAct, 8> op{X, scale, bias, out};
-            return run<8, 4>(view(g), op, ws, st, bias, bias ? f : 0);
+            return run<8, 4>(gv, op, ws, st, bias, bias ? f : 0);
         }
         case 128: {
             SumBf16Op<kAct, 4> op{X, scale, bias, out};
-            return run<8, 4>(view(g), op, ws, st, bias, bias ? f : 0);
+            return run<8, 4>(gv, op, ws, st, bias, bias ? f : 0);
         }
         case 64: {
             SumBf16Op<kAct, 2> op{X, scale, bias, out};
-            return run<8, 4>(view(g), op, ws, st, bias, bias ? f : 0);
+            return run<8, 4>(gv, op, ws, st, bias, bias ? f : 0);
         }
     }
     return cudaErrorInvalidValue;
@@ -979,13 +1004,17 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
 
 cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
                                 __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(g, Y, f, g.dinv, bias, out, ws, st);
-    return agg_sum_bf16<SAGA_ACT_NONE>(g, Y, f, g.dinv, bias, out, ws, st);
+    // with the aggregation view the GEMM epilogue has finished the self-loop-only
+    // and empty rows; the rest run over the compacted CSR (rmap -> output row)
+    const GraphView gv = g.arow ? view_agg(g) : view(g);
+    const float *scale = g.arow ? g.adinv : g.dinv;
+    if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(gv, Y, f, scale, bias, out, ws, st);
+    return agg_sum_bf16<SAGA_ACT_NONE>(gv, Y, f, scale, bias, out, ws, st);
 }
 
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
                                  AggWorkspace ws, cudaStream_t st) {
-    return agg_sum_bf16<SAGA_ACT_NONE>(g, X, f, g.inv_deg, nullptr, M, ws, st);
+    return agg_sum_bf16<SAGA_ACT_NONE>(view(g), X, f, g.inv_deg, nullptr, M, ws, st);
 }
 
 cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
@@ -1001,8 +1030,15 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    GatOp op{z, el, er, slope, out};
-    return run<8, 5>(view_fine(g), op, ws, st);  // 48 registers, 40 warps per SM: 3% faster than 4 blocks
+    // with the aggregation view the GEMM epilogue has written the rows whose only
+    // in-edge is the self-loop (or with none); the rest run over the compacted CSR
+    // 48 registers, 40 warps per SM: 3% faster than 4 blocks.  With the
+    // aggregation view (the GEMM epilogue has written ELU(z) of the rows whose
+    // only in-edge is the self-loop, and 0 for rows without one) the kernel
+    // runs over the other rows only: C3 gat_edge 205 -> 183 us for +9 us of
+    // GEMM output stores.
+    if (g.arow) return run<8, 5>(view_agg_fine(g), GatOp<true>{z, el, er, slope, out, g.arow}, ws, st);
+    return run<8, 5>(view_fine(g), GatOp<false>{z, el, er, slope, out, nullptr}, ws, st);
 }
 
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, double *Sx,

@@ -55,6 +55,7 @@ struct Layout {
             : (kSmemLimit - 1024 - (int)sizeof(Barriers) - kBBytes - kCBytes) / kATileBytes;
     static constexpr int kBytes = 1024 + kBBytes + kStages * kATileBytes + kCBytes + (int)sizeof(Barriers);
     static_assert(kStages >= 2, "not enough shared memory for the A ring");
+    static_assert(BN != 256 || kStages >= 4, "the BN = 256 GEMM (C5) keeps a 4-stage A ring");
 };
 
 struct EpiParams {
@@ -64,6 +65,7 @@ struct EpiParams {
     int act;
     const float *a_src, *a_dst;
     float *el, *er;
+    bool self_out;  // the aggregation view's self-term output tile (GemmArgs::out2; kernel template SELF)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -74,11 +76,14 @@ __device__ __forceinline__ float act_fn(float x, int act) {
     return x;
 }
 
-template <int BN>
+// EPI (GemmEpi) and SELF (the aggregation view's self-term output tile) are
+// compile-time: a runtime epilogue switch let the compiler interleave the
+// modes' code and made the C5 GEMM 3.5x slower.
+template <int BN, int EPI, bool SELF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
-                   const __grid_constant__ CUtensorMap tmC, const __nv_bfloat16 *__restrict__ W, int64_t M, int KB,
-                   int KB0, EpiParams ep) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmO,
+                   const __nv_bfloat16 *__restrict__ W, int64_t M, int KB, int KB0, EpiParams ep) {
     using L = Layout<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -106,11 +111,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmA0);
         ptx::prefetch_tmap(&tmA1);
         ptx::prefetch_tmap(&tmC);
+        ptx::prefetch_tmap(&tmO);
     }
     for (int i = threadIdx.x; i < BN; i += kThreads) {
-        if (ep.epi == EPI_BIAS_ACT) {
+        if constexpr (EPI == EPI_BIAS_ACT || (EPI == EPI_ROWSCALE && SELF)) {
             bar->vec[i] = ep.bias ? ep.bias[i] : 0.0f;
-        } else if (ep.epi == EPI_GAT) {  // BN = 64 here
+        } else if constexpr (EPI == EPI_GAT) {  // BN = 64 here
             bar->vec[i] = ep.a_src[i];
             bar->vec[64 + i] = ep.a_dst[i];
         }
@@ -248,16 +254,100 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row = m0 + r;
             const bool valid = row < M;
             float scale = 1.0f;
-            if (ep.epi == EPI_ROWSCALE) scale = valid ? __ldg(ep.row_scale + row) : 0.0f;
+            if constexpr (EPI == EPI_ROWSCALE) scale = valid ? __ldg(ep.row_scale + row) : 0.0f;
+            // GAT: a row whose only in-edge is its self-loop has one softmax term of
+            // weight 1, so its output is ELU(z[v]); a row without in-edges gets 0
+            const float gcoef = EPI == EPI_GAT && SELF && valid && __ldg(ep.row_scale + row) > 0.0f ? 1.0f : 0.0f;
             ptx::mbar_wait(&bar->tfull[acc], aphase);
             ptx::tc_fence_after();
             float el[8], er[8];
-            if (ep.epi == EPI_GAT) {
+            if constexpr (EPI == EPI_GAT) {
 #pragma unroll
                 for (int h = 0; h < 8; ++h) el[h] = er[h] = 0.0f;
             }
 #pragma unroll 1
             for (int c64 = 0; c64 < BN / 64; ++c64) {
+                if constexpr (SELF) {
+                    // GCN with the aggregation view: the Y chunk and the output chunk
+                    // act(scale Y + b) of EVERY row -- the layer output of a row whose
+                    // in-edges are one self-loop (or none), from the same bf16 Y the
+                    // aggregation would sum; the view's rows overwrite theirs later --
+                    // are packed in registers and staged in the two buffers for two
+                    // TMA tile stores (single-buffered: the wait for the previous
+                    // chunk's stores overlaps this chunk's math).  Measured at C5
+                    // (GEMM ms): these tile stores 1.16-1.25; storing only the rows
+                    // needed -- per-row copies by the 4 epilogue warps 1.36-1.78, TMA
+                    // scatter4 of the compacted rows 4.0 (issue-bound).
+                    if constexpr (EPI == EPI_GAT) {
+                        // one 64-column chunk per tile: wait for the previous tile's
+                        // stores first, then stage each half straight away (fewer live
+                        // registers next to el / er)
+                        if (et == 0) ptx::bulk_wait_read<0>();
+                        named_bar(1, 128);
+                    }
+                    uint32_t yp[32], op[32];
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const int col0 = c64 * 64 + half * 32;
+                        uint32_t v[32];
+                        ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col0, v);
+                        ptx::tmem_ld_wait();
+                        if constexpr (EPI == EPI_GAT) {  // BN = 64: el / er from the fp32 accumulators
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const int h = (half * 32 + i) >> 3;
+                                el[h] = fmaf(__uint_as_float(v[i]), bar->vec[col0 + i], el[h]);
+                                er[h] = fmaf(__uint_as_float(v[i]), bar->vec[64 + col0 + i], er[h]);
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const uint32_t y2 = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * scale,
+                                                                 __uint_as_float(v[2 * i + 1]) * scale);
+                            const float2 f = ptx::unpack_bf16x2(y2);
+                            yp[half * 16 + i] = y2;
+                            if constexpr (EPI == EPI_GAT) {  // ELU as the edge kernel's flush (output bf16)
+                                const float a = gcoef * f.x, b = gcoef * f.y;
+                                op[half * 16 + i] = ptx::pack_bf16x2(a > 0.0f ? a : __expf(a) - 1.0f,
+                                                                     b > 0.0f ? b : __expf(b) - 1.0f);
+                            } else {
+                                op[half * 16 + i] =
+                                    ptx::pack_bf16x2(act_fn(fmaf(scale, f.x, bar->vec[col0 + 2 * i]), ep.act),
+                                                     act_fn(fmaf(scale, f.y, bar->vec[col0 + 2 * i + 1]), ep.act));
+                            }
+                        }
+                        if constexpr (EPI == EPI_GAT) {
+#pragma unroll
+                            for (int c4 = 0; c4 < 4; ++c4) {
+                                const int ch = half * 4 + c4, off = r * 128 + ((ch ^ (r & 7)) << 4);
+                                const int b = half * 16 + 4 * c4;
+                                *reinterpret_cast<uint4 *>(Cs + off) = make_uint4(yp[b], yp[b + 1], yp[b + 2], yp[b + 3]);
+                                *reinterpret_cast<uint4 *>(Cs + kCStageBytes + off) =
+                                    make_uint4(op[b], op[b + 1], op[b + 2], op[b + 3]);
+                            }
+                        }
+                    }
+                    if constexpr (EPI != EPI_GAT) {
+                        if (et == 0) ptx::bulk_wait_read<0>();  // the previous chunk's stores have read both buffers
+                        named_bar(1, 128);
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch) {
+                            const int off = r * 128 + ((ch ^ (r & 7)) << 4);
+                            *reinterpret_cast<uint4 *>(Cs + off) =
+                                make_uint4(yp[4 * ch], yp[4 * ch + 1], yp[4 * ch + 2], yp[4 * ch + 3]);
+                            *reinterpret_cast<uint4 *>(Cs + kCStageBytes + off) =
+                                make_uint4(op[4 * ch], op[4 * ch + 1], op[4 * ch + 2], op[4 * ch + 3]);
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();
+                    named_bar(1, 128);
+                    if (et == 0) {
+                        ptx::tma_store_2d(&tmC, Cs, c64 * 64, (int32_t)m0);
+                        ptx::tma_store_2d(&tmO, Cs + kCStageBytes, c64 * 64, (int32_t)m0);
+                        ptx::bulk_commit();
+                    }
+                    continue;
+                }
                 uint8_t *stg = Cs + (cstage & 1) * kCStageBytes;
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
@@ -268,10 +358,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float x[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
-                    if (ep.epi == EPI_ROWSCALE) {
+                    if constexpr (EPI == EPI_ROWSCALE) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) x[i] *= scale;
-                    } else if (ep.epi == EPI_BIAS_ACT) {
+                    } else if constexpr (EPI == EPI_BIAS_ACT) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) x[i] = act_fn(x[i] + bar->vec[col0 + i], ep.act);
                     } else {  // EPI_GAT: heads of 8 columns; el/er from the fp32 accumulators
@@ -305,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // accumulator drained: hand it back to the MMA warp
             ptx::tc_fence_before();
             ptx::mbar_arrive(&bar->tempty[acc]);
-            if (ep.epi == EPI_GAT && valid) {
+            if (EPI == EPI_GAT && valid) {
                 float4 *pe = reinterpret_cast<float4 *>(ep.el + row * 8);
                 float4 *pr = reinterpret_cast<float4 *>(ep.er + row * 8);
                 pe[0] = make_float4(el[0], el[1], el[2], el[3]);
@@ -343,30 +433,31 @@ EncodeFn get_encode() {
 }
 
 
-template <int BN>
+template <int BN, int EPI, bool SELF>
 cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorMap &mc,
-                      int KB, int KB0, const EpiParams &ep, cudaStream_t st) {
+                      const CUtensorMap &mo, int KB, int KB0, const EpiParams &ep, cudaStream_t st) {
     using L = Layout<BN>;
     // per launch: the attribute is per device, and the call is cheap next to the kernel
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_gemm_bf16_tc<BN, EPI, SELF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e) return e;
     const int64_t ntiles = (a.M + kBM - 1) / kBM;
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-    return launch(k_gemm_bf16_tc<BN>, grid, kThreads, L::kBytes, st, m0, m1, mc, a.W, a.M, KB, KB0, ep);
+    return launch(k_gemm_bf16_tc<BN, EPI, SELF>, grid, kThreads, L::kBytes, st, m0, m1, mc, mo, a.W, a.M, KB, KB0, ep);
 }
 
 }  // namespace
 
-// 2-D bf16 row-major [rows][cols] map with a {64 col, 128 row} box, 128B swizzle.
-bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols) {
+// 2-D bf16 row-major [rows][cols] map with a {64 col, box_rows row} box, 128B swizzle.
+bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int box_rows) {  // box_rows <= 256
     EncodeFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -380,18 +471,36 @@ cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char *
         *why = "GEMM K must be a multiple of 64 and <= 256";
         return cudaErrorInvalidValue;
     }
-    CUtensorMap m0, m1, mc;
+    CUtensorMap m0, m1, mc, mo;
     if (!make_map_bf16(&m0, a.A0, a.M, a.K0) || !make_map_bf16(&m1, a.K1 ? a.A1 : a.A0, a.M, a.K1 ? a.K1 : a.K0) ||
-        !make_map_bf16(&mc, a.out, a.M, a.N)) {
+        !make_map_bf16(&mc, a.out, a.M, a.N) || !make_map_bf16(&mo, a.out2 ? a.out2 : a.out, a.M, a.N)) {
         *why = "cuTensorMapEncodeTiled failed";
         return cudaErrorInvalidValue;
     }
-    EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er};
+    EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er,
+                 (a.epi == EPI_ROWSCALE || a.epi == EPI_GAT) && a.out2};
     const int KB = K / kBK, KB0 = a.K0 / kBK;
-    switch (a.N) {
-        case 256: return launch_bn<256>(a, m0, m1, mc, KB, KB0, ep, st);
-        case 128: return launch_bn<128>(a, m0, m1, mc, KB, KB0, ep, st);
-        case 64: return launch_bn<64>(a, m0, m1, mc, KB, KB0, ep, st);
+    // instantiated modes: GCN (row scale, with / without the self-term output),
+    // SAGE / LSTM (bias + act), GAT (N = 64, with / without)
+    const bool self = ep.self_out;
+    if (a.epi == EPI_ROWSCALE) {
+        switch (a.N) {
+            case 256: return self ? launch_bn<256, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
+                                  : launch_bn<256, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 128: return self ? launch_bn<128, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
+                                  : launch_bn<128, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 64: return self ? launch_bn<64, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
+                                 : launch_bn<64, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+        }
+    } else if (a.epi == EPI_BIAS_ACT) {
+        switch (a.N) {
+            case 256: return launch_bn<256, EPI_BIAS_ACT, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 128: return launch_bn<128, EPI_BIAS_ACT, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 64: return launch_bn<64, EPI_BIAS_ACT, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+        }
+    } else if (a.N == 64) {
+        return self ? launch_bn<64, EPI_GAT, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
+                    : launch_bn<64, EPI_GAT, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
     }
     *why = "GEMM N must be 64, 128 or 256";
     return cudaErrorInvalidValue;

@@ -380,6 +380,38 @@ __global__ void k_heavy_slots(int32_t nh, const int32_t *__restrict__ deg_order,
     if (s < nh) heavy_slot[deg_order[s]] = s;
 }
 
+// Step 8 (aggregation view): per vertex, whether its in-edges are nothing but
+// one self-loop (or none): then the GCN output needs no gather.
+__global__ void k_epi_flags(int32_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_src,
+                            const int32_t *__restrict__ in_deg, int32_t *aflag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t d = in_deg[v];
+        aflag[v] = (d == 0 || (d == 1 && col_src[row_ptr[v]] == (int32_t)v)) ? 0 : 1;
+    }
+}
+__global__ void k_compact_rows(int32_t n, const int32_t *__restrict__ aflag, const int64_t *__restrict__ apos,
+                               const int32_t *__restrict__ in_deg, const float *__restrict__ dinv, int32_t *arow,
+                               int32_t *adeg, float *adinv) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (!aflag[v]) continue;
+        const int64_t i = apos[v];
+        arow[i] = (int32_t)v;
+        adeg[i] = in_deg[v];
+        adinv[i] = dinv[v];
+    }
+}
+// warp per compact row: its in-edges, in CSR order
+__global__ void k_compact_edges(int32_t an, const int32_t *__restrict__ arow, const int64_t *__restrict__ row_ptr,
+                                const int32_t *__restrict__ col_src, const int64_t *__restrict__ arow_ptr,
+                                int32_t *acol_src) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < an;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = row_ptr[arow[i]], d = arow_ptr[i + 1] - arow_ptr[i], o = arow_ptr[i];
+        for (int64_t k = lane; k < d; k += 32) acol_src[o + k] = col_src[b + k];
+    }
+}
+
 __global__ void k_degree_desc_keys(int32_t n, const int32_t *__restrict__ in_deg, int32_t *keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         keys[i] = 0x7FFFFFFF - in_deg[i];
@@ -472,6 +504,56 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     SAGA_TRY(merge_path_schedule(n, e, g->row_ptr, &g->task_items, &g->ntasks, &g->task_v, &g->task_p, st, 32));
     SAGA_TRY(merge_path_schedule(n, e, g->row_ptr, &g->ftask_items, &g->fntasks, &g->ftask_v, &g->ftask_p, st, 128));
 
+    // 8. aggregation view (see GraphDev): rows with only a self-loop or no
+    //    in-edge are finished by the GCN GEMM epilogue; a compacted CSR of the
+    //    others (a second host sync, for its sizes)
+    if (n > 0) {
+        int32_t *aflag, *adeg = nullptr;
+        int64_t *apos;
+        SAGA_TRY(cudaMallocAsync(&aflag, sizeof(int32_t) * nn, st));
+        SAGA_TRY(cudaMallocAsync(&apos, sizeof(int64_t) * (nn + 1), st));
+        k_epi_flags<<<grid_for(n, 256), 256, 0, st>>>(n, g->row_ptr, g->col_src, g->in_deg, aflag);
+        SAGA_TRY(cudaGetLastError());
+        SAGA_TRY(scan_exclusive<int32_t>(aflag, n, apos, st));
+        int64_t an = 0;
+        SAGA_TRY(cudaMemcpyAsync(&an, apos + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SAGA_TRY(cudaStreamSynchronize(st));
+        if (an < n) {
+            g->an = (int32_t)an;
+            const size_t na = (size_t)std::max<int64_t>(an, 1);
+            SAGA_TRY(cudaMallocAsync(&g->arow, sizeof(int32_t) * na, st));
+            SAGA_TRY(cudaMallocAsync(&g->adinv, sizeof(float) * na, st));
+            SAGA_TRY(cudaMallocAsync(&g->arow_ptr, sizeof(int64_t) * (na + 1), st));
+            SAGA_TRY(cudaMallocAsync(&adeg, sizeof(int32_t) * na, st));
+            k_compact_rows<<<grid_for(n, 256), 256, 0, st>>>(n, aflag, apos, g->in_deg, g->dinv, g->arow, adeg,
+                                                             g->adinv);
+            SAGA_TRY(cudaGetLastError());
+            SAGA_TRY(scan_exclusive<int32_t>(adeg, an, g->arow_ptr, st));
+            // every skipped row with an in-edge has exactly one (its self-loop)
+            int64_t skipped_edges = 0;
+            {
+                int64_t tot = 0;
+                SAGA_TRY(cudaMemcpyAsync(&tot, g->arow_ptr + an, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+                SAGA_TRY(cudaStreamSynchronize(st));
+                g->ae = tot;
+                skipped_edges = e - tot;
+                (void)skipped_edges;
+            }
+            SAGA_TRY(cudaMallocAsync(&g->acol_src, sizeof(int32_t) * (size_t)std::max<int64_t>(g->ae, 1), st));
+            if (an > 0)
+                k_compact_edges<<<grid_for(an * 32, 256), 256, 0, st>>>(g->an, g->arow, g->row_ptr, g->col_src,
+                                                                        g->arow_ptr, g->acol_src);
+            SAGA_TRY(cudaGetLastError());
+            SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->atask_items, &g->antasks, &g->atask_v,
+                                         &g->atask_p, st, 32));
+            SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->aftask_items, &g->afntasks, &g->aftask_v,
+                                         &g->aftask_p, st, 128));
+            cudaFreeAsync(adeg, st);
+        }
+        cudaFreeAsync(aflag, st);
+        cudaFreeAsync(apos, st);
+    }
+
     // 7. typed view: rows (v, t), edges in (dst, type, COO index) order
     if (etype && n > 0) {
         const int32_t T = g->num_etypes;
@@ -512,7 +594,8 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
 void free_graph(GraphDev *g) {
     cudaStream_t st = g->stream;
     void *ptrs[] = {g->row_ptr,  g->col_src,  g->edge_id,  g->etype,   g->in_deg,  g->out_deg, g->dinv,
-                    g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->trow_ptr, g->tcol_src, g->tinv_deg,
+                    g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->arow, g->arow_ptr,
+                    g->acol_src, g->adinv, g->atask_v, g->atask_p, g->aftask_v, g->aftask_p, g->trow_ptr, g->tcol_src, g->tinv_deg,
                     g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, st);

@@ -95,6 +95,22 @@ struct GraphDev {
     int64_t ttask_items = 0, tntasks = 0;
     int32_t *ttask_v = nullptr;
     int64_t *ttask_p = nullptr;
+    // Aggregation view (built when some rows' in-edges are nothing but one
+    // self-loop, or none): those rows' GCN output act(dinv[v] Y[v] + b)
+    // is written by the GEMM epilogue, and the aggregation runs over a
+    // compacted CSR of the other rows only (row i = vertex arow[i]).
+    int32_t an = 0;               // host: aggregation rows
+    int64_t ae = 0;               // host: their in-edges
+    int32_t *arow = nullptr;      // [an]  vertex of compact row i
+    int64_t *arow_ptr = nullptr;  // [an+1]
+    int32_t *acol_src = nullptr;  // [ae]
+    float *adinv = nullptr;       // [an]  dinv[arow[i]]
+    int64_t atask_items = 0, antasks = 0;
+    int32_t *atask_v = nullptr;
+    int64_t *atask_p = nullptr;
+    int64_t aftask_items = 0, afntasks = 0;  // the 4x finer schedule of the view (GAT)
+    int32_t *aftask_v = nullptr;
+    int64_t *aftask_p = nullptr;
     cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
 };
 
@@ -146,6 +162,12 @@ struct GemmArgs {
     __nv_bfloat16 *out = nullptr;                      // [M][N]
     GemmEpi epi = EPI_ROWSCALE;
     const float *row_scale = nullptr;                  // EPI_ROWSCALE
+    // Optional with the aggregation view (rows whose in-edges are one self-loop
+    // or none; the view's rows overwrite theirs later), for every row:
+    //   EPI_ROWSCALE (GCN): out2[v] = act(row_scale[v] Y[v] + bias)  (bf16 Y, [M][N])
+    //   EPI_GAT: out2[v] = ELU(z[v]) if row_scale[v] > 0 (one in-edge, the
+    //            self-loop: a single softmax term), else 0   (bf16 z, [M][64])
+    __nv_bfloat16 *out2 = nullptr;
     const float *bias = nullptr;                       // EPI_BIAS_ACT
     int act = 0;
     const float *a_src = nullptr, *a_dst = nullptr;    // EPI_GAT [heads][8]
@@ -174,8 +196,8 @@ cudaError_t launch_gru_heavy_f64(const GraphDev &g, const HeavyWs &w, const floa
 // GGNN (NEXT-4): AB = H . [W_a | W_b] + [0 | b_e] (split-TF32, also splits the
 // GRU weights into wsplit), the edge-MLP gather m = sum|max act(A[u] + B[v]),
 // and the GRU GEMM over [m || h].
-// 2-D bf16 row-major [rows][cols] tensor map, {64 col, 128 row} box, 128B swizzle (gemm_tc.cu).
-bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols);
+// 2-D bf16 row-major [rows][cols] tensor map, {64 col, box_rows row} box, 128B swizzle (gemm_tc.cu).
+bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int box_rows = 128);
 
 // NEXT-1: GraphSAGE-mean aggregation fused with its tcgen05 concat-GEMM
 // (sage_fused.cu); img = workspace for the staged W^T image.

@@ -165,7 +165,7 @@ struct Plan {
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
     Plan p;
     // the typed gathers run over the typed view's own schedule
-    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks});
+    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks, g.antasks, g.afntasks});
     const size_t n = (size_t)g.n;
     size_t width = 0;
     switch (kind) {
@@ -442,7 +442,8 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     // split-row tickets start at 0; every ticket's winner resets its counter,
     // so a completed call leaves them zero (opts.workspace_zeroed skips this)
     if (!o.workspace_zeroed && !(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {
-        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks}), st);
+        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks, d.antasks, d.afntasks}),
+                            st);
         if (e) return cuda_fail(e, "memset counters");
     }
     const char *why = "";
@@ -468,6 +469,11 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.out = Y;
             a.epi = EPI_ROWSCALE;
             a.row_scale = d.dinv;
+            if (d.arow) {  // the epilogue finishes the self-loop-only / empty rows (aggregation view)
+                a.out2 = static_cast<__nv_bfloat16 *>(out->data);
+                a.bias = w->bias;
+                a.act = o.act;
+            }
             {
                 ProfScope ps_("gemm_bf16_tc", st);
                 e = launch_gemm_bf16_tc(a, st, &why);
@@ -524,6 +530,10 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.out = z;
             a.epi = EPI_GAT;
             a.a_src = w->attn_src; a.a_dst = w->attn_dst; a.el = el; a.er = er;
+            if (d.arow) {  // the epilogue writes ELU(z) of the self-loop-only rows (aggregation view)
+                a.row_scale = d.dinv;
+                a.out2 = static_cast<__nv_bfloat16 *>(out->data);
+            }
             {
                 ProfScope ps_("gemm_bf16_tc_gat", st);
                 e = launch_gemm_bf16_tc(a, st, &why);

@@ -7,7 +7,7 @@ fi
 for c in $2; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/b_$c.json 2>gpurun_out/b_$c.err;
   python -c "import json;j=json.load(open('gpurun_out/b_$c.json'));print('$c', round(j['ms_per_step'],4), {k:round(v['avg_ms'],4) for k,v in j['config']['per_kernel'].items()})" || tail -5 gpurun_out/b_$c.err; done
 if [ -n "$3" ]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_$3.csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 40 --csv --log-file gpurun_out/launches_$3.csv \
     python bench.py --config $3 --steps 2 --warmup 3 --no-cpu --e2e-steps 0 --no-kernel-events > /dev/null 2>&1
   python - "$3" <<'PY'
 import csv, sys, collections
