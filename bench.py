@@ -50,6 +50,69 @@ def ncu_traffic(cfg_name, kernel):
         return None
 
 
+def ncu_traffic_source():
+    """Where `traffic` comes from: the capture file and the commit it was taken at."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        j = json.load(open(p))
+        return f"profiles/ncu_traffic.json (ncu --set full, commit {j.get('_commit', 'unknown')}, {j.get('_when', '')})"
+    except Exception:
+        return None
+
+
+def measured_tensor_peaks(dev):
+    """TF32 and INT8 dense tensor-core throughput measured in this run (torch /
+    cuBLAS, 8192^3, best of 5): the roofline peaks of the split-TF32 and the
+    int8-sliced GEMMs (MEASURED_PEAKS.json has bf16 only)."""
+    out = {}
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        old = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        out["tf32_tflops"] = _best_tflops(lambda: a @ b, 2.0 * n ** 3)
+        torch.backends.cuda.matmul.allow_tf32 = old
+        ai = torch.randint(-64, 64, (n, n), device=dev, dtype=torch.int8)
+        bi = torch.randint(-64, 64, (n, n), device=dev, dtype=torch.int8).t()
+        out["int8_tops"] = _best_tflops(lambda: torch._int_mm(ai, bi), 2.0 * n ** 3)
+        del a, b, ai, bi
+    except Exception as e:  # pragma: no cover
+        out["error"] = str(e)[:120]
+    return out
+
+
+def _best_tflops(fn, flops, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        t = s.elapsed_time(e) / 1e3
+        best = t if best is None else min(best, t)
+    return flops / best / 1e12
+
+
+def graph_stats(cfg, d):
+    """Sizes of the graph's aggregation view (graph_build.cu step 8) for the
+    byte model: rows whose in-edges are one self-loop or none are finished by
+    the GEMM epilogue; the gather runs over the other rows' edges and reads
+    each distinct source row once at least."""
+    src, dst = d["src"].long(), d["dst"].long()
+    n = cfg.n
+    indeg = torch.bincount(dst, minlength=n)
+    loops = torch.bincount(dst[src == dst], minlength=n)
+    epi = (indeg == 0) | ((indeg == 1) & (loops == 1))
+    keep = ~epi[dst]
+    srcs = torch.unique(src[keep])
+    return {"n_epi": int(epi.sum()), "an": int((~epi).sum()), "ae": int(keep.sum()), "n_src": int(srcs.numel()),
+            "n_heavy": int((indeg >= 256).sum())}  # kHeavyInDeg: the fp64 ApplyVertex rows (gru_f64.cu)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -112,12 +175,14 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- byte model ----
-def algorithmic(cfg):
+def algorithmic(cfg, gs=None):
     """Algorithmic (compulsory) bytes and FLOPs PER LAUNCH of each kernel
     (DESIGN.md section 5): every array the kernel must touch, once; FLOPs are
     the layer's own arithmetic counted once.  `peak` names the roofline the
     kernel is held to: "hbm", or "tensor_bf16" / "tensor_tf32x3" (3xTF32: the
-    fp32-accurate product costs three TF32 MMAs, so its peak is TF32 / 3)."""
+    fp32-accurate product costs three TF32 MMAs, so its peak is TF32 / 3).
+    `gs` (graph_stats): the aggregation view's sizes (GAT) and the heavy rows
+    (gated, GGNN)."""
     n, e = cfg.n, cfg.num_edges
     out = {}
     if cfg.model == "gcn" and cfg.dtype == "bf16":
@@ -142,10 +207,15 @@ def algorithmic(cfg):
                                "flops": 2 * n * (2 * f0 * f1 + 2 * f1 * f2) // 2, "peak": "tensor_bf16"}
     elif cfg.model == "gat":
         fi, fo = cfg.dims
-        out["gemm_bf16_tc_gat"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * fo * 2 + n * 64, "flops": 2 * n * fi * fo,
-                                   "peak": "tensor_bf16"}
-        out["gat_edge"] = {"bytes": e * 4 + (n + 1) * 8 + n * fo * 2 + n * 64 + n * fo * 2, "flops": 10 * e * fo,
-                           "peak": "hbm"}
+        if gs is None:
+            gs = {"n_epi": 0, "an": n, "ae": e, "n_src": n}
+        an, ae = gs["an"], gs["ae"]
+        # GEMM: X, W read; z and el / er of every row written, the epilogue rows' outputs
+        out["gemm_bf16_tc_gat"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * fo * 2 + n * 64 + gs["n_epi"] * fo * 2,
+                                   "flops": 2 * n * fi * fo, "peak": "tensor_bf16"}
+        # view gather: col_src, row_ptr, row map, er of its rows; z and el of each gathered source once; outputs
+        out["gat_edge"] = {"bytes": ae * 4 + (an + 1) * 8 + an * 4 + an * 32 + gs["n_src"] * (fo * 2 + 32)
+                           + an * fo * 2, "flops": 10 * ae * fo, "peak": "hbm"}
     elif cfg.model == "gated":
         f, T = cfg.dims[0], cfg.num_etypes
         # typed view (rows (v, t)): col_src, row_ptr of n*T rows, H once, S [n][T][f]
@@ -154,7 +224,10 @@ def algorithmic(cfg):
         # S read, m written + read, h read twice (GEMM A operand, GRU epilogue), h' written
         out["gated_apply_tf32x3"] = {"bytes": n * T * f * 4 + n * f * 4 * 5, "flops": 2 * n * (T * f * f + 6 * f * f),
                                      "peak": "tensor_tf32x3"}
-        out["gated_apply_sgemm"] = dict(out["gated_apply_tf32x3"], peak="hbm")
+        if gs:  # heavy rows: fp64 message GEMM + GRU from the fp64 sums (gru_f64.cu)
+            nh = gs["n_heavy"]
+            out["gru_heavy_f64"] = {"bytes": nh * (T * f * 8 + f * 4 * 2 + 4) + (T + 6) * f * f * (4 + 8),
+                                    "flops": 2 * nh * (T * f * f + 6 * f * f), "peak": "fp64_pipe"}
     elif cfg.model == "sage_lstm":
         f, fo = cfg.dims
         # per edge: gather a 1 KB row of P (4 gates bf16); recurrent GEMV 2 * 4f * f FLOPs
@@ -174,9 +247,10 @@ def algorithmic(cfg):
                                     "peak": "tensor_tf32x3"}
     elif cfg.model == "ggnn":
         f = cfg.dims[0]
-        # AB = H . [W_a | W_b] + [0 | b_e]: H read, AB written (K = f, N = 2f)
-        out["ggnn_edge_tf32x3"] = {"bytes": n * f * 4 + n * 2 * f * 4, "flops": 2 * n * f * 2 * f,
-                                   "peak": "tensor_tf32x3"}
+        # AB = H . [W_a | W_b] + [0 | b_e] on the int8 tensor cores (exact accumulation):
+        # H read, AB written (K = f, N = 2f); 8 int8 MMAs per product
+        out["ggnn_edge_i8x"] = {"bytes": n * f * 4 + n * 2 * f * 4, "flops": 2 * n * f * 2 * f,
+                                "peak": "tensor_i8x8"}
         # compulsory: col_src, row_ptr, AB read once (A and B halves), m written
         # (the per-edge A-row gathers, 512 B each, are L2 traffic, as for the
         # other gathers)
@@ -184,10 +258,17 @@ def algorithmic(cfg):
                                    "flops": 3 * e * f, "peak": "hbm"}
         # GRU over [m || h]: m, h read (h twice), h' written
         out["ggnn_gru_tf32x3"] = {"bytes": n * f * 4 * 4, "flops": 2 * n * 6 * f * f, "peak": "tensor_tf32x3"}
+        if gs:  # heavy rows in fp64: their B before the gather, the GRU after it (gru_f64.cu)
+            nh = gs["n_heavy"]
+            out["ggnn_heavy_b_f64"] = {"bytes": nh * (f * 4 + f * 8) + 7 * f * f * (4 + 8), "flops": 2 * nh * f * f,
+                                       "peak": "fp64_pipe"}
+            out["gru_heavy_f64"] = {"bytes": nh * (f * 8 + f * 4 * 2 + 4) + 6 * f * f * 8,
+                                    "flops": 2 * nh * 6 * f * f, "peak": "fp64_pipe"}
     return out
 
 
 FMA_PIPE_TFLOPS = 148 * 4 * 16 * 2 * 1.965e9 / 1e12
+FP64_PIPE_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
 def roofline_of(name, spec, avg_s, pk, traffic):
@@ -200,6 +281,11 @@ def roofline_of(name, spec, avg_s, pk, traffic):
         if traffic:  # DRAM-throughput fraction: the ncu bytes this kernel really moves, at this launch time
             r["dram_frac"] = traffic / avg_s / 1e9 / pk["hbm_gbs"]
         return r
+    if spec["peak"] == "fp64_pipe":
+        peak = FP64_PIPE_TFLOPS
+        ach = spec["flops"] / avg_s / 1e12
+        return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
+                    peak_note="derived: 148 SM x 64 DFMA/clk x 2 FLOP x 1.965 GHz (CUDA-core FP64)")
     if spec["peak"] == "fma_pipe":
         # CUDA-core FMA pipe: 148 SMs x 4 SMSPs x 32 lanes / (reciprocal throughput 2 cycles per
         # warp FMA, B300_MICROARCH "Pipe rates") x 2 FLOP x 1.965 GHz = 37.2 TFLOP/s
@@ -207,12 +293,20 @@ def roofline_of(name, spec, avg_s, pk, traffic):
         ach = spec["flops"] / avg_s / 1e12
         return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
                     peak_note="derived: 148 SM x 4 SMSP x 16 FMA/clk x 2 FLOP x 1.965 GHz (FHFMA.BF16 on the FMA pipe)")
-    # tensor: bf16 measured burst peak; TF32 = bf16 x (1.1 / 2.25 nominal ratio); 3xTF32 = TF32 / 3
+    # tensor: bf16 measured burst peak (MEASURED_PEAKS.json); TF32 and INT8 measured
+    # in this run (cuBLAS 8192^3, measured_tensor_peaks), else the nominal ratios
     peak = pk["bf16_tflops"]
     note = "measured bf16 burst"
     if spec["peak"] == "tensor_tf32x3":
-        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
-        note = "measured bf16 burst x nominal tf32/bf16 (1.1/2.25) / 3 (3xTF32)"
+        if pk.get("tf32_tflops"):
+            peak, note = pk["tf32_tflops"] / 3.0, "TF32 measured in this run / 3 (3xTF32)"
+        else:
+            peak, note = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0, "bf16 x nominal tf32/bf16 (1.1/2.25) / 3 (3xTF32)"
+    elif spec["peak"] == "tensor_i8x8":
+        if pk.get("int8_tops"):
+            peak, note = pk["int8_tops"] / 8.0, "INT8 measured in this run / 8 (8 digit-pair MMAs per product)"
+        else:
+            peak, note = pk["bf16_tflops"] * 2.0 / 8.0, "bf16 x nominal int8/bf16 (2) / 8 (digit-pair MMAs)"
     # a contraction whose bytes take longer than its FLOPs is HBM-bound
     if spec["bytes"] / (pk["hbm_gbs"] * 1e9) > spec["flops"] / (peak * 1e12):
         ach = spec["bytes"] / avg_s / 1e9
@@ -410,32 +504,37 @@ def run_saga(args, cfg):
         H.gpu_step(saga, cfg, g, d, layers, outs)
     torch.cuda.synchronize()
 
-    # Two timed regions of the same K steps (each step: L2 flush if the inputs
-    # fit in L2, start event, the layer step, end event), each captured ONCE
-    # into a CUDA graph and replayed once, so host launch overhead is out of
-    # the timed steps.  Region 1 holds only the step events: `value` and
-    # `ms_per_step`.  Region 2 adds the per-kernel event pairs (saga_profile)
-    # as timing nodes of its graph, i.e. the kernel durations behind
-    # `per_kernel` and `roofline` are measured live over a timed region; those
-    # nodes serialise the kernels (~3-5 us each), so region 2's step time is
-    # reported separately (`ms_per_step_profiled`).  --eager launches both
-    # sequences directly.
+    # Timed regions of the same K steps (each step: L2 flush if the inputs fit
+    # in L2, start event, the layer step, end event), each captured ONCE into a
+    # CUDA graph and replayed once, so host launch overhead is out of the timed
+    # steps (--eager launches them directly).
+    #   1. only the step events: `value`, `ms_per_step` (mean), median / min;
+    #   2. per-kernel event pairs around EVERY kernel (saga_profile): the
+    #      `per_kernel` table; the pairs serialise the kernels and turn off
+    #      programmatic launch, so these durations are upper bounds
+    #      (`ms_per_step_profiled` is that region's step time);
+    #   3. event pairs around the dominant kernel ONLY (saga_profile_filter),
+    #      every other kernel launched exactly as in region 1 (PDL on): the
+    #      roofline's kernel time;
+    #   4. C1-C4, C6-C8 (inputs fit in L2): region 1 without the L2 flush --
+    #      steady-state inference with a warm L2 (`warm_l2`).
     stream = torch.cuda.current_stream()
     ext = {} if args.eager else {"external": True}
 
-    def region(profiled):
+    def region(profiled, only=None, do_flush=True):
         starts = [torch.cuda.Event(enable_timing=True, **ext) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True, **ext) for _ in range(args.steps)]
 
         def timed_steps():
             for i in range(args.steps):
-                if flush is not None:
+                if flush is not None and do_flush:
                     flush.zero_()
                 starts[i].record()
                 H.gpu_step(saga, cfg, g, d, layers, outs)
                 ends[i].record()
 
         graph = None
+        saga.saga_profile_filter(only)
         saga.saga_profile_enable(profiled and not args.no_kernel_events)
         if not args.eager:
             torch.cuda.synchronize()
@@ -452,29 +551,39 @@ def run_saga(args, cfg):
         torch.cuda.synchronize()
         prof = saga.saga_profile_read()
         saga.saga_profile_enable(False)
+        saga.saga_profile_filter(None)
         if ws > 1:
             torch.distributed.barrier()
-        return max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dev), prof
+        return [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)], prof
 
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.15)
-    tot_ms, _ = region(False)
-    tot_prof_ms, prof = region(True)
+    step_ms, _ = region(False)
+    tot_ms = max_over_ranks(sum(step_ms), dev)
+    prof_ms, prof = region(True)
+    tot_prof_ms = max_over_ranks(sum(prof_ms), dev)
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    dom_prof = region(True, only=dom)[1] if dom and not args.no_kernel_events else {}
+    warm_ms = region(False, do_flush=False)[0] if flush is not None else None
     clocks = clk.stop()
     upd_step = cfg.layer_updates()
     value = job_value(upd_step, args.steps, ws, tot_ms)
     launches = sum(n for n, _ in prof.values())
 
-    # roofline of the dominant kernel (largest share of the step)
-    alg = algorithmic(cfg)
-    pk = peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    # roofline of the dominant kernel (largest share of the step), timed in region 3
+    gs = graph_stats(cfg, d) if cfg.model in ("gat", "gated", "ggnn") else None
+    alg = algorithmic(cfg, gs)
+    pk = dict(peaks(), **measured_tensor_peaks(dev))
     roof = None
     if dom and dom in alg:
-        n_l, ms_l = prof[dom]
+        n_l, ms_l = dom_prof.get(dom, prof[dom])
         traffic = args.traffic if args.traffic is not None else ncu_traffic(cfg.name, dom)
         roof = roofline_of(dom, alg[dom], ms_l / n_l / 1e3, pk, traffic)
+        roof["kernel_ms_serialised"] = prof[dom][1] / prof[dom][0]
+        roof["kernel_time"] = ("region 3: CUDA events around this kernel only, every other kernel as in the "
+                               "timed step (programmatic launch on)")
+        roof["traffic_source"] = ncu_traffic_source() if traffic is not None else None
     kernels = {}
     for k, (n_l, ms_l) in prof.items():
         a = alg.get(k, {"bytes": 0, "flops": 0})
@@ -499,6 +608,14 @@ def run_saga(args, cfg):
     conf = workload_config(cfg)
     conf.update({"l2": "inputs larger than L2 (no flush)" if big else "512 MiB L2 flush between steps (untimed)",
                  "graph_build_ms": build_ms, "per_kernel": kernels,
+                 "step_ms": {"mean": tot_ms / args.steps, "median": statistics.median(step_ms), "min": min(step_ms),
+                             "max": max(step_ms)},
+                 "warm_l2": None if warm_ms is None else {
+                     "what": "the same K steps without the L2 flush (steady-state, inputs L2-resident)",
+                     "mean_ms": sum(warm_ms) / len(warm_ms), "median_ms": statistics.median(warm_ms),
+                     "min_ms": min(warm_ms),
+                     "value": job_value(upd_step, args.steps, ws, max_over_ranks(sum(warm_ms), dev))},
+                 "graph_view": gs, "peaks": pk,
                  "ms_per_step_profiled": tot_prof_ms / args.steps,
                  "launch": "eager" if args.eager else "CUDA graph: the K timed steps captured once, replayed once"})
     res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

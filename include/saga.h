@@ -234,6 +234,11 @@ SAGA_API void saga_free(saga_graph *g);
  * Costs two event records per launch; disabled by default.
  */
 SAGA_API saga_status saga_profile_enable(int enable);
+/* Restrict the brackets to the launches with this label (NULL or "" = all).
+ * With a filter, the unbracketed kernels keep their programmatic dependent
+ * launches, so the bracketed kernel is timed inside an otherwise unchanged
+ * step (its own launch is serialised by the event records). */
+SAGA_API saga_status saga_profile_filter(const char *label);
 SAGA_API int32_t saga_profile_count(void);
 SAGA_API saga_status saga_profile_get(int32_t index, const char **name, int64_t *launches, double *total_ms);
 

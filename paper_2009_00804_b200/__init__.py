@@ -32,7 +32,7 @@ MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GAT
 # Every symbol include/saga.h declares (checked by tests/test_abi.py).
 EXPORTS = ["saga_abi_version", "saga_graph_build", "saga_graph_info", "saga_graph_copy_csr",
            "saga_layer_workspace_bytes", "saga_layer", "saga_free", "saga_last_error",
-           "saga_profile_enable", "saga_profile_count", "saga_profile_get"]
+           "saga_profile_enable", "saga_profile_filter", "saga_profile_count", "saga_profile_get"]
 
 
 class SagaError(RuntimeError):
@@ -84,6 +84,8 @@ def _load():
     L.saga_last_error.argtypes = []
     L.saga_profile_enable.restype = ctypes.c_int
     L.saga_profile_enable.argtypes = [ctypes.c_int]
+    L.saga_profile_filter.restype = ctypes.c_int
+    L.saga_profile_filter.argtypes = [ctypes.c_char_p]
     L.saga_profile_count.restype = ctypes.c_int32
     L.saga_profile_count.argtypes = []
     L.saga_profile_get.restype = ctypes.c_int
@@ -102,6 +104,11 @@ def saga_abi_version() -> int:
 def saga_profile_enable(enable: bool = True):
     """Per-kernel CUDA-event timing inside saga_layer (resets the counters)."""
     _check(_lib.saga_profile_enable(1 if enable else 0))
+
+
+def saga_profile_filter(label=None):
+    """Bracket only the launches labelled `label` (None: all); the others keep PDL."""
+    _check(_lib.saga_profile_filter(label.encode() if label else None))
 
 
 def saga_profile_read() -> dict:

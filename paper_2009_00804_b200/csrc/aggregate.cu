@@ -73,12 +73,8 @@ GraphView view_typed(const GraphDev &g) {
     return GraphView{g.trow_ptr, g.tcol_src, g.ttask_v, g.ttask_p, g.ttask_items, g.tntasks,
                      g.n * g.num_etypes, (int32_t)g.e, nullptr};
 }
-// the aggregation rows only (graph_build.cu step 8): rows whose in-edges are
-// nothing but one self-loop, or none, are finished by the GEMM epilogue
-GraphView view_agg(const GraphDev &g) {
-    return GraphView{g.arow_ptr, g.acol_src, g.atask_v, g.atask_p, g.atask_items, g.antasks, g.an, (int32_t)g.ae,
-                     g.arow};
-}
+// the aggregation rows only (graph_build.cu step 8; GAT): rows whose in-edges
+// are nothing but one self-loop, or none, are finished by the GEMM epilogue
 GraphView view_agg_fine(const GraphDev &g) {
     return GraphView{g.arow_ptr, g.acol_src, g.aftask_v, g.aftask_p, g.aftask_items, g.afntasks, g.an, (int32_t)g.ae,
                      g.arow};
@@ -1004,12 +1000,11 @@ size_t agg_partial_floats(saga_model kind, int32_t width, int32_t heads) {
 
 cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32_t f, const float *bias, int act,
                                 __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    // with the aggregation view the GEMM epilogue has finished the self-loop-only
-    // and empty rows; the rest run over the compacted CSR (rmap -> output row)
-    const GraphView gv = g.arow ? view_agg(g) : view(g);
-    const float *scale = g.arow ? g.adinv : g.dinv;
-    if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(gv, Y, f, scale, bias, out, ws, st);
-    return agg_sum_bf16<SAGA_ACT_NONE>(gv, Y, f, scale, bias, out, ws, st);
+    // (The aggregation view -- the GEMM epilogue finishing the rows whose only
+    // in-edge is the self-loop -- measured no faster at C5: the gather lost
+    // 0.6-0.8 ms but the GEMM gained 0.45-0.5 ms of output stores.)
+    if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(view(g), Y, f, g.dinv, bias, out, ws, st);
+    return agg_sum_bf16<SAGA_ACT_NONE>(view(g), Y, f, g.dinv, bias, out, ws, st);
 }
 
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,

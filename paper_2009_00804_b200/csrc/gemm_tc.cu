@@ -65,7 +65,7 @@ struct EpiParams {
     int act;
     const float *a_src, *a_dst;
     float *el, *er;
-    bool self_out;  // the aggregation view's self-term output tile (GemmArgs::out2; kernel template SELF)
+    bool self_out;  // GAT: the aggregation view's output tile (GemmArgs::out2; kernel template SELF)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmO);
     }
     for (int i = threadIdx.x; i < BN; i += kThreads) {
-        if constexpr (EPI == EPI_BIAS_ACT || (EPI == EPI_ROWSCALE && SELF)) {
+        if constexpr (EPI == EPI_BIAS_ACT) {
             bar->vec[i] = ep.bias ? ep.bias[i] : 0.0f;
         } else if constexpr (EPI == EPI_GAT) {  // BN = 64 here
             bar->vec[i] = ep.a_src[i];
@@ -268,23 +268,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int c64 = 0; c64 < BN / 64; ++c64) {
                 if constexpr (SELF) {
-                    // GCN with the aggregation view: the Y chunk and the output chunk
-                    // act(scale Y + b) of EVERY row -- the layer output of a row whose
-                    // in-edges are one self-loop (or none), from the same bf16 Y the
-                    // aggregation would sum; the view's rows overwrite theirs later --
-                    // are packed in registers and staged in the two buffers for two
-                    // TMA tile stores (single-buffered: the wait for the previous
-                    // chunk's stores overlaps this chunk's math).  Measured at C5
-                    // (GEMM ms): these tile stores 1.16-1.25; storing only the rows
-                    // needed -- per-row copies by the 4 epilogue warps 1.36-1.78, TMA
-                    // scatter4 of the compacted rows 4.0 (issue-bound).
-                    if constexpr (EPI == EPI_GAT) {
-                        // one 64-column chunk per tile: wait for the previous tile's
-                        // stores first, then stage each half straight away (fewer live
-                        // registers next to el / er)
-                        if (et == 0) ptx::bulk_wait_read<0>();
-                        named_bar(1, 128);
-                    }
+                    // GAT with the aggregation view: the z chunk and the output chunk
+                    // of EVERY row -- ELU(z[v]) for a row whose only in-edge is its
+                    // self-loop (one softmax term of weight 1), 0 for a row with
+                    // none, from the same bf16 z the edge kernel would read; the
+                    // view's rows overwrite theirs -- staged in the two buffers for
+                    // two TMA tile stores (+33 MB at C3, gat_edge 205 -> 183 us).
+                    // The same for GCN (act(dinv Y + b)) was measured at C5: the
+                    // gather lost 0.6-0.8 ms, the GEMM gained 0.45-0.5 ms of stores
+                    // (per-row stores of only the needed rows were slower still:
+                    // from the epilogue warps 1.36-1.78 ms, 4 dedicated store warps
+                    // 1.41, TMA scatter4 4.0, vs 1.16-1.25 for the tile stores).
                     uint32_t yp[32], op[32];
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
@@ -292,51 +286,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t v[32];
                         ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col0, v);
                         ptx::tmem_ld_wait();
-                        if constexpr (EPI == EPI_GAT) {  // BN = 64: el / er from the fp32 accumulators
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                const int h = (half * 32 + i) >> 3;
-                                el[h] = fmaf(__uint_as_float(v[i]), bar->vec[col0 + i], el[h]);
-                                er[h] = fmaf(__uint_as_float(v[i]), bar->vec[64 + col0 + i], er[h]);
-                            }
+                        for (int i = 0; i < 32; ++i) {  // BN = 64: el / er from the fp32 accumulators
+                            const int h = (half * 32 + i) >> 3;
+                            el[h] = fmaf(__uint_as_float(v[i]), bar->vec[col0 + i], el[h]);
+                            er[h] = fmaf(__uint_as_float(v[i]), bar->vec[64 + col0 + i], er[h]);
                         }
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            const uint32_t y2 = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * scale,
-                                                                 __uint_as_float(v[2 * i + 1]) * scale);
+                            const uint32_t y2 =
+                                ptx::pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
                             const float2 f = ptx::unpack_bf16x2(y2);
                             yp[half * 16 + i] = y2;
-                            if constexpr (EPI == EPI_GAT) {  // ELU as the edge kernel's flush (output bf16)
-                                const float a = gcoef * f.x, b = gcoef * f.y;
-                                op[half * 16 + i] = ptx::pack_bf16x2(a > 0.0f ? a : __expf(a) - 1.0f,
-                                                                     b > 0.0f ? b : __expf(b) - 1.0f);
-                            } else {
-                                op[half * 16 + i] =
-                                    ptx::pack_bf16x2(act_fn(fmaf(scale, f.x, bar->vec[col0 + 2 * i]), ep.act),
-                                                     act_fn(fmaf(scale, f.y, bar->vec[col0 + 2 * i + 1]), ep.act));
-                            }
+                            // ELU as the edge kernel's flush (output bf16)
+                            const float a = gcoef * f.x, b = gcoef * f.y;
+                            op[half * 16 + i] = ptx::pack_bf16x2(a > 0.0f ? a : __expf(a) - 1.0f,
+                                                                 b > 0.0f ? b : __expf(b) - 1.0f);
                         }
-                        if constexpr (EPI == EPI_GAT) {
 #pragma unroll
-                            for (int c4 = 0; c4 < 4; ++c4) {
-                                const int ch = half * 4 + c4, off = r * 128 + ((ch ^ (r & 7)) << 4);
-                                const int b = half * 16 + 4 * c4;
-                                *reinterpret_cast<uint4 *>(Cs + off) = make_uint4(yp[b], yp[b + 1], yp[b + 2], yp[b + 3]);
-                                *reinterpret_cast<uint4 *>(Cs + kCStageBytes + off) =
-                                    make_uint4(op[b], op[b + 1], op[b + 2], op[b + 3]);
-                            }
-                        }
-                    }
-                    if constexpr (EPI != EPI_GAT) {
-                        if (et == 0) ptx::bulk_wait_read<0>();  // the previous chunk's stores have read both buffers
-                        named_bar(1, 128);
-#pragma unroll
-                        for (int ch = 0; ch < 8; ++ch) {
-                            const int off = r * 128 + ((ch ^ (r & 7)) << 4);
-                            *reinterpret_cast<uint4 *>(Cs + off) =
-                                make_uint4(yp[4 * ch], yp[4 * ch + 1], yp[4 * ch + 2], yp[4 * ch + 3]);
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const int ch = half * 4 + c4, off = r * 128 + ((ch ^ (r & 7)) << 4);
+                            const int b = half * 16 + 4 * c4;
+                            *reinterpret_cast<uint4 *>(Cs + off) = make_uint4(yp[b], yp[b + 1], yp[b + 2], yp[b + 3]);
                             *reinterpret_cast<uint4 *>(Cs + kCStageBytes + off) =
-                                make_uint4(op[4 * ch], op[4 * ch + 1], op[4 * ch + 2], op[4 * ch + 3]);
+                                make_uint4(op[b], op[b + 1], op[b + 2], op[b + 3]);
                         }
                     }
                     ptx::fence_proxy_async_smem();
@@ -478,19 +451,16 @@ cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char *
         return cudaErrorInvalidValue;
     }
     EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er,
-                 (a.epi == EPI_ROWSCALE || a.epi == EPI_GAT) && a.out2};
+                 a.epi == EPI_GAT && a.out2};
     const int KB = K / kBK, KB0 = a.K0 / kBK;
-    // instantiated modes: GCN (row scale, with / without the self-term output),
-    // SAGE / LSTM (bias + act), GAT (N = 64, with / without)
+    // instantiated modes: GCN (row scale), SAGE / LSTM (bias + act), GAT (N = 64,
+    // with / without the aggregation view's output tile)
     const bool self = ep.self_out;
     if (a.epi == EPI_ROWSCALE) {
         switch (a.N) {
-            case 256: return self ? launch_bn<256, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
-                                  : launch_bn<256, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
-            case 128: return self ? launch_bn<128, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
-                                  : launch_bn<128, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
-            case 64: return self ? launch_bn<64, EPI_ROWSCALE, true>(a, m0, m1, mc, mo, KB, KB0, ep, st)
-                                 : launch_bn<64, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 256: return launch_bn<256, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 128: return launch_bn<128, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
+            case 64: return launch_bn<64, EPI_ROWSCALE, false>(a, m0, m1, mc, mo, KB, KB0, ep, st);
         }
     } else if (a.epi == EPI_BIAS_ACT) {
         switch (a.N) {

@@ -544,8 +544,6 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
                 k_compact_edges<<<grid_for(an * 32, 256), 256, 0, st>>>(g->an, g->arow, g->row_ptr, g->col_src,
                                                                         g->arow_ptr, g->acol_src);
             SAGA_TRY(cudaGetLastError());
-            SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->atask_items, &g->antasks, &g->atask_v,
-                                         &g->atask_p, st, 32));
             SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->aftask_items, &g->afntasks, &g->aftask_v,
                                          &g->aftask_p, st, 128));
             cudaFreeAsync(adeg, st);
@@ -595,7 +593,7 @@ void free_graph(GraphDev *g) {
     cudaStream_t st = g->stream;
     void *ptrs[] = {g->row_ptr,  g->col_src,  g->edge_id,  g->etype,   g->in_deg,  g->out_deg, g->dinv,
                     g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->arow, g->arow_ptr,
-                    g->acol_src, g->adinv, g->atask_v, g->atask_p, g->aftask_v, g->aftask_p, g->trow_ptr, g->tcol_src, g->tinv_deg,
+                    g->acol_src, g->adinv, g->aftask_v, g->aftask_p, g->trow_ptr, g->tcol_src, g->tinv_deg,
                     g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, st);

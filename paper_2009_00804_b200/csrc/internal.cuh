@@ -96,19 +96,16 @@ struct GraphDev {
     int32_t *ttask_v = nullptr;
     int64_t *ttask_p = nullptr;
     // Aggregation view (built when some rows' in-edges are nothing but one
-    // self-loop, or none): those rows' GCN output act(dinv[v] Y[v] + b)
-    // is written by the GEMM epilogue, and the aggregation runs over a
-    // compacted CSR of the other rows only (row i = vertex arow[i]).
+    // self-loop, or none): those rows' GAT output (ELU(z[v]), or 0) is written
+    // by the GEMM epilogue, and the edge softmax runs over a compacted CSR of
+    // the other rows only (row i = vertex arow[i]).
     int32_t an = 0;               // host: aggregation rows
     int64_t ae = 0;               // host: their in-edges
     int32_t *arow = nullptr;      // [an]  vertex of compact row i
     int64_t *arow_ptr = nullptr;  // [an+1]
     int32_t *acol_src = nullptr;  // [ae]
     float *adinv = nullptr;       // [an]  dinv[arow[i]]
-    int64_t atask_items = 0, antasks = 0;
-    int32_t *atask_v = nullptr;
-    int64_t *atask_p = nullptr;
-    int64_t aftask_items = 0, afntasks = 0;  // the 4x finer schedule of the view (GAT)
+    int64_t aftask_items = 0, afntasks = 0;  // its merge-path schedule (the 4x finer one, GAT)
     int32_t *aftask_v = nullptr;
     int64_t *aftask_p = nullptr;
     cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
@@ -162,11 +159,9 @@ struct GemmArgs {
     __nv_bfloat16 *out = nullptr;                      // [M][N]
     GemmEpi epi = EPI_ROWSCALE;
     const float *row_scale = nullptr;                  // EPI_ROWSCALE
-    // Optional with the aggregation view (rows whose in-edges are one self-loop
-    // or none; the view's rows overwrite theirs later), for every row:
-    //   EPI_ROWSCALE (GCN): out2[v] = act(row_scale[v] Y[v] + bias)  (bf16 Y, [M][N])
-    //   EPI_GAT: out2[v] = ELU(z[v]) if row_scale[v] > 0 (one in-edge, the
-    //            self-loop: a single softmax term), else 0   (bf16 z, [M][64])
+    // EPI_GAT, optional with the aggregation view: for every row out2[v] =
+    // ELU(z[v]) if row_scale[v] > 0 (one in-edge, the self-loop: a single
+    // softmax term), else 0 (bf16 z, [M][64]); the view's rows overwrite theirs
     __nv_bfloat16 *out2 = nullptr;
     const float *bias = nullptr;                       // EPI_BIAS_ACT
     int act = 0;

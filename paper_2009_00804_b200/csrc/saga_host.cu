@@ -53,6 +53,7 @@ struct ProfRec {
 struct Prof {
     std::mutex mu;
     bool on = false;
+    std::string only;  // non-empty: bracket only the launches with this label (PDL stays on for the rest)
     std::vector<std::string> names;
     std::vector<int64_t> launches;
     std::vector<double> ms;
@@ -99,7 +100,7 @@ struct ProfScope {
     cudaStream_t st;
     ProfScope(const char *name, cudaStream_t s) : on(false), st(s) {
         std::lock_guard<std::mutex> lk(g_prof.mu);
-        if (!g_prof.on) return;
+        if (!g_prof.on || (!g_prof.only.empty() && g_prof.only != name)) return;
         on = true;
         r.name = g_prof.id(name);
         r.a = g_prof.get();
@@ -130,7 +131,7 @@ struct PdlCall {
         bool prof;
         {
             std::lock_guard<std::mutex> lk(g_prof.mu);
-            prof = g_prof.on;
+            prof = g_prof.on && g_prof.only.empty();  // a filtered profile keeps PDL for the other kernels
         }
         saga::g_pdl_call = !off && !prof;
         saga::g_pdl_armed = false;
@@ -165,7 +166,7 @@ struct Plan {
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
     Plan p;
     // the typed gathers run over the typed view's own schedule
-    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks, g.antasks, g.afntasks});
+    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks, g.afntasks});
     const size_t n = (size_t)g.n;
     size_t width = 0;
     switch (kind) {
@@ -380,6 +381,12 @@ saga_status saga_profile_enable(int enable) {
     return SAGA_OK;
 }
 
+saga_status saga_profile_filter(const char *label) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.only = label ? label : "";
+    return SAGA_OK;
+}
+
 int32_t saga_profile_count(void) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     return (int32_t)g_prof.names.size();
@@ -442,7 +449,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     // split-row tickets start at 0; every ticket's winner resets its counter,
     // so a completed call leaves them zero (opts.workspace_zeroed skips this)
     if (!o.workspace_zeroed && !(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {
-        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks, d.antasks, d.afntasks}),
+        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks, d.afntasks}),
                             st);
         if (e) return cuda_fail(e, "memset counters");
     }
@@ -469,11 +476,6 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             a.out = Y;
             a.epi = EPI_ROWSCALE;
             a.row_scale = d.dinv;
-            if (d.arow) {  // the epilogue finishes the self-loop-only / empty rows (aggregation view)
-                a.out2 = static_cast<__nv_bfloat16 *>(out->data);
-                a.bias = w->bias;
-                a.act = o.act;
-            }
             {
                 ProfScope ps_("gemm_bf16_tc", st);
                 e = launch_gemm_bf16_tc(a, st, &why);

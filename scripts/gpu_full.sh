@@ -3,7 +3,7 @@
 # Usage (on the GPU box): bash scripts/gpu_full.sh <tag>
 TAG=${1:-r1}
 mkdir -p gpurun_out/$TAG
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/$TAG/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/$TAG/pytest_gpu.log
+SAGA_PARITY_LOG=gpurun_out/$TAG/parity.json timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/$TAG/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/$TAG/pytest_gpu.log
 tail -2 gpurun_out/$TAG/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/$TAG/smoke.log 2>&1; tail -1 gpurun_out/$TAG/smoke.log
 timeout 900 python bench.py > gpurun_out/$TAG/bench_C5.json 2> gpurun_out/$TAG/bench_C5.err
@@ -16,7 +16,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_launch.log 2>&1
 for c in C5 C3 C4 C2 C1 C6 C7 C8; do
   timeout 300 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/plain_$c.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'segreduce|rowwise|gemm|lstm_gather' -s 2 -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'segreduce|rowwise|gemm|lstm_gather|slice|heavy|weights_f64|split' -s 3 -c 9 \
       -o gpurun_out/$TAG/full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_full_$c.log 2>&1
 done
 ls gpurun_out/$TAG

@@ -1,6 +1,6 @@
 """Summarise a gpurun measurement pass (scripts/gpu_full.sh) into profiles/.
 
-  python scripts/make_profiles.py <tag>
+  python scripts/make_profiles.py <tag> [<commit>]
 
 Writes profiles/<tag>_ncu_summary.md (per config and kernel: duration, DRAM
 read/write bytes, L2 hit rate, occupancy, issue activity, top stall reasons),
@@ -20,13 +20,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)]
     "C1": [("GcnF32FusedOp", "gcn_f32_fused")],
     "C2": [("SumBf16Op", "agg_mean_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
-    "C3": [("GatDenseOp", "gat_edge"), ("GatOp", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
-    "C4": [("SumF32Op", "agg_typed_f32"), ("TypedF32Op", "agg_typed_f32"), ("k_sgemm", "gated_apply_sgemm"), ("k_gemm_tf32split", "gated_apply_tf32x3")],
+    "C3": [("GatOp", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
+    "C4": [("SumF32Op", "agg_typed_f32"), ("k_gemm_tf32split", "gated_apply_tf32x3"), ("k_split_weights", "gated_apply_tf32x3"),
+           ("k_gru_heavy_f64", "gru_heavy_f64"), ("k_weights_f64", "gru_heavy_f64")],
     "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
-    "C6": [("SumF32Op", "agg_typed_mean_f32"), ("TypedF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3")],
-    "C7": [("k_lstm_gather", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
+    "C6": [("SumF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3"), ("k_split_rgcn", "rgcn_apply_tf32x3")],
+    "C7": [("k_lstm_gather", "lstm_gather"), ("k_stage_whh", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C8": [("EdgeMlpOp", "agg_edge_mlp_f32"), ("k_gemm_tf32split<256", "ggnn_gru_tf32x3"),
-           ("k_gemm_tf32split<128", "ggnn_edge_tf32x3")],
+           ("k_gemm_i8x", "ggnn_edge_i8x"), ("k_slice_rows", "ggnn_edge_i8x"), ("k_slice_wt_ggnn", "ggnn_edge_i8x"),
+           ("k_split_ggnn", "ggnn_split_weights"), ("k_ggnn_heavy_b", "ggnn_heavy_b_f64"),
+           ("k_weights_f64", "ggnn_heavy_b_f64"), ("k_gru_heavy_f64", "gru_heavy_f64")],
 }
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram_read"),
         ("dram__bytes_write.sum", "dram_write"), ("lts__t_sector_hit_rate.pct", "L2_hit_%"),
@@ -78,7 +81,7 @@ def read_rep(path):
     return rows
 
 
-def main(tag):
+def main(tag, commit="unknown"):
     src = os.path.join(ROOT, "gpurun_out", tag)
     dst = os.path.join(ROOT, "profiles")
     os.makedirs(dst, exist_ok=True)
@@ -92,7 +95,7 @@ def main(tag):
         md.append(f"\n## {cfg}\n")
         md.append("| kernel | label | ms | DRAM read GB | DRAM write GB | L2 hit % | DRAM thr % | tensor % | warps act % | issue % | regs | top stalls |")
         md.append("|---|---|---|---|---|---|---|---|---|---|---|---|")
-        per = defaultdict(list)
+        per = defaultdict(lambda: defaultdict(list))  # label -> kernel name -> DRAM bytes per launch
         for d in read_rep(rep):
             lab = label_of(cfg, d["name"])
             short = d["name"].split("(")[0][:60]
@@ -101,8 +104,11 @@ def main(tag):
                       f"{d.get('tensor_pipe_%', 0):.1f} | {d.get('warps_active_%', 0):.1f} | {d.get('issue_active_%', 0):.1f} | "
                       f"{d.get('regs', 0):.0f} | {d['stalls']} |")
             if lab:
-                per[lab].append(d.get("dram_read", 0) + d.get("dram_write", 0))
-        traffic[cfg] = {lab: sum(v) / len(v) for lab, v in per.items()}
+                per[lab][d["name"].split("(")[0]].append(d.get("dram_read", 0) + d.get("dram_write", 0))
+        # a label's traffic per call: the mean of each of its kernels, summed over its kernels
+        traffic[cfg] = {lab: sum(sum(v) / len(v) for v in ks.values()) for lab, ks in per.items()}
+    traffic["_commit"] = commit
+    traffic["_when"] = tag
     open(os.path.join(dst, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     # launch list of the default bench command: shares per kernel
@@ -131,11 +137,11 @@ def main(tag):
         b = os.path.join(src, f"bench_{cfg}.json")
         if os.path.exists(b):
             shutil.copy(b, os.path.join(dst, f"{tag}_bench_{cfg}.json"))
-    for extra in ["bench_ref_C5.json", "pytest_gpu.log", "smoke.log"]:
+    for extra in ["bench_ref_C5.json", "pytest_gpu.log", "smoke.log", "parity.json"]:
         b = os.path.join(src, extra)
         if os.path.exists(b):
             shutil.copy(b, os.path.join(dst, f"{tag}_{extra}"))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "unknown")

@@ -31,13 +31,26 @@ def test_c5_aggregation_compulsory_bytes(bench):
     assert g["flops"] == 2 * n * 256 * 256
 
 
+def test_gat_view_bytes(bench):
+    """GAT with the aggregation view (graph_build.cu step 8): the edge kernel's
+    rows, edges and gathered sources only; the GEMM also writes the epilogue
+    rows' outputs."""
+    c = W.CONFIGS["C3"]
+    n = c.n
+    gs = {"n_epi": 100, "an": 900, "ae": 5000, "n_src": 700, "n_heavy": 0}
+    a = bench.algorithmic(c, gs)["gat_edge"]
+    assert a["bytes"] == 4 * 5000 + 8 * 901 + 4 * 900 + 32 * 900 + 700 * (128 + 32) + 900 * 128
+    g = bench.algorithmic(c, gs)["gemm_bf16_tc_gat"]
+    assert g["bytes"] == n * 512 + 256 * 64 * 2 + n * 128 + n * 64 + 100 * 128
+
+
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"])
 def test_every_profiled_kernel_has_a_model(bench, cfg):
     expected = {"C1": {"gcn_f32_fused"}, "C2": {"agg_mean_bf16", "gemm_bf16_tc"},
                 "C3": {"gemm_bf16_tc_gat", "gat_edge"}, "C4": {"agg_typed_f32", "gated_apply_tf32x3"},
                 "C5": {"gemm_bf16_tc", "agg_gcn_bf16"}, "C6": {"agg_typed_mean_f32", "rgcn_apply_tf32x3"},
                 "C7": {"lstm_gather", "lstm_input_gemm", "gemm_bf16_tc"},
-                "C8": {"ggnn_edge_tf32x3", "agg_edge_mlp_f32", "ggnn_gru_tf32x3"}}[cfg]
+                "C8": {"ggnn_edge_i8x", "agg_edge_mlp_f32", "ggnn_gru_tf32x3"}}[cfg]
     alg = bench.algorithmic(W.CONFIGS[cfg])
     assert expected <= set(alg)
     for k in expected:
