@@ -38,6 +38,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -167,12 +168,18 @@ struct SumBf16Op {
 // weight dinv[u] per edge, then the ApplyVertex GEMV (W staged in shared
 // memory) fused into the row flush, spread over the warp (lane L computes
 // outputs L and L + 32).
-template <int NPL>
+// kRowwise (graphs whose in-degrees are all <= kRowwiseMaxDeg, one warp per
+// row): fp32 accumulation -- a sum of <= 64 terms is within ~4e-6 of fp64,
+// and the fp32 -> fp64 conversions (XU pipe) were 12% of C1's stalls.
+template <int NPL, bool kRowwise = false>
 struct GcnF32FusedOp {
     static constexpr int kWin = 1;
     static constexpr int kSlot = 2 * 32 * NPL;  // doubles as float pairs
     __device__ static int win_col(int) { return 0; }
-    struct Acc { double a[NPL]; };  // fp64 accumulation (see SumF32Op)
+    using AccT = typename std::conditional<kRowwise, float, double>::type;
+    struct Acc { AccT a[NPL]; };  // merge-path: fp64 accumulation (see SumF32Op)
+    // W [f_in][f_out] elements per thread of a 256-thread block (f_in <= 32 NPL, f_out <= 64)
+    static constexpr int kWPerThread = 8 * NPL;
     struct Val { float x[NPL]; float w; };
     const float *X;
     int32_t f_in, f_out;
@@ -204,12 +211,12 @@ struct GcnF32FusedOp {
     }
     __device__ __forceinline__ void add(Acc &c, const Val &v, float) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c.a[i] = fma((double)v.w, (double)v.x[i], c.a[i]);
+        for (int i = 0; i < NPL; ++i) c.a[i] = fma((AccT)v.w, (AccT)v.x[i], c.a[i]);
     }
     __device__ __forceinline__ void finish_w(int32_t v, const Acc &c, float rs, const float *Ws, int lane) const {
         float h[NPL];
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) h[i] = (float)((double)rs * c.a[i]);
+        for (int i = 0; i < NPL; ++i) h[i] = (float)((AccT)rs * c.a[i]);
         if (f_out <= 16) {
             // narrow outputs (C1: 64 -> 16): lane = (k half, column); each half
             // runs its own dependent FMA chains over half the inputs (one per
@@ -248,11 +255,11 @@ struct GcnF32FusedOp {
     }
     __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) reinterpret_cast<double *>(slot)[lane * NPL + i] = c.a[i];
+        for (int i = 0; i < NPL; ++i) reinterpret_cast<double *>(slot)[lane * NPL + i] = (double)c.a[i];
     }
     __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c.a[i] += __ldcg(reinterpret_cast<const double *>(slot) + lane * NPL + i);
+        for (int i = 0; i < NPL; ++i) c.a[i] += (AccT)__ldcg(reinterpret_cast<const double *>(slot) + lane * NPL + i);
     }
 };
 
@@ -916,23 +923,25 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
                                                          const int32_t *__restrict__ col_src, int32_t n, const Op op,
                                                          const float *Wg, const int32_t w_elems) {
     extern __shared__ float Ws[];
+    constexpr int kWReg = Op::kWPerThread;  // W elements per thread in flight (w_elems <= kWReg * kBlock)
     const int lane = threadIdx.x & 31;
     int32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    // the first row's bounds are in flight while the block stages W
-    int32_t p0 = r < n ? (int32_t)__ldg(row_ptr + r) : 0, p1 = r < n ? (int32_t)__ldg(row_ptr + r + 1) : 0;
+    const bool first = r < n;
     griddep_launch();
-    if (Wg) {
-        for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
-        __syncthreads();
+    // the block's W loads are issued first and stay in flight (registers)
+    // while the first row is gathered: W is only needed by the epilogue GEMV.
+    // (Staging W before the gather put its DRAM round trip in series with the
+    // row's three: 23% of C1's stall samples waited on it.)
+    float wreg[kWReg];
+#pragma unroll
+    for (int k = 0; k < kWReg; ++k) {
+        const int i = threadIdx.x + k * kBlock;
+        wreg[k] = i < w_elems ? __ldg(Wg + i) : 0.0f;
     }
     griddep_wait();
-    for (; r < n; r += gridDim.x * kWarpsPerBlock) {
-        if (r != blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) {
-            p0 = (int32_t)__ldg(row_ptr + r);
-            p1 = (int32_t)__ldg(row_ptr + r + 1);
-        }
-        const float rs = op.row_value(r, 0);
-        typename Op::Acc acc;
+    auto gather = [&](int32_t row, typename Op::Acc &acc, float &rs) {
+        const int32_t p0 = (int32_t)__ldg(row_ptr + row), p1 = (int32_t)__ldg(row_ptr + row + 1);
+        rs = op.row_value(row, 0);
         op.zero(acc);
         for (int32_t q0 = p0; q0 < p1; q0 += 32) {
             const int32_t cnt = min(32, p1 - q0);
@@ -946,6 +955,19 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
                     if (j + u < cnt) op.add(acc, val[u], rs);
             }
         }
+    };
+    typename Op::Acc acc;
+    float rs = 0.0f;
+    if (first) gather(r, acc, rs);
+#pragma unroll
+    for (int k = 0; k < kWReg; ++k) {
+        const int i = threadIdx.x + k * kBlock;
+        if (i < w_elems) Ws[i] = wreg[k];
+    }
+    __syncthreads();
+    if (first) do_finish(op, r, acc, rs, lane, Ws, 0);
+    for (r += gridDim.x * kWarpsPerBlock; r < n; r += gridDim.x * kWarpsPerBlock) {
+        gather(r, acc, rs);
         do_finish(op, r, acc, rs, lane, Ws, 0);
     }
 }
@@ -973,13 +995,14 @@ cudaError_t agg_sum_bf16(const GraphView &gv, const __nv_bfloat16 *X, int32_t f,
 template <int NPL>
 cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,
                     const float *bias, int act, float *out, AggWorkspace ws, cudaStream_t st) {
-    GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
     if (gcn_f32_rowwise(g)) {
         if (g.n == 0) return cudaSuccess;
+        GcnF32FusedOp<NPL, true> op{X, f_in, f_out, g.dinv, bias, act, out};
         const unsigned blocks = (unsigned)((g.n + kWarpsPerBlock - 1) / kWarpsPerBlock);
-        return launch(k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL>>, blocks, kBlock,
+        return launch(k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL, true>>, blocks, kBlock,
                       sizeof(float) * f_in * f_out, st, g.row_ptr, g.col_src, g.n, op, W, f_in * f_out);
     }
+    GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
     return run<8, NPL == 4 ? 2 : 3>(view(g), op, ws, st, W, f_in * f_out);
 }
 
