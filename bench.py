@@ -267,7 +267,7 @@ def algorithmic(cfg, gs=None):
     return out
 
 
-FMA_PIPE_TFLOPS = 148 * 4 * 16 * 2 * 1.965e9 / 1e12
+FMA_PIPE_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 FP64_PIPE_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
@@ -287,12 +287,14 @@ def roofline_of(name, spec, avg_s, pk, traffic):
         return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
                     peak_note="derived: 148 SM x 64 DFMA/clk x 2 FLOP x 1.965 GHz (CUDA-core FP64)")
     if spec["peak"] == "fma_pipe":
-        # CUDA-core FMA pipe: 148 SMs x 4 SMSPs x 32 lanes / (reciprocal throughput 2 cycles per
-        # warp FMA, B300_MICROARCH "Pipe rates") x 2 FLOP x 1.965 GHz = 37.2 TFLOP/s
+        # the full-rate FP32 FMA pipe: 148 SMs x 128 FMA/clk x 2 FLOP x 1.965 GHz = 74.4 TFLOP/s.
+        # (Round 1 held the LSTM gather to the half-rate FHFMA.BF16 instruction it uses, 37.2 --
+        # the kernel's own choice, not the machine's bound.)
         peak = FMA_PIPE_TFLOPS
         ach = spec["flops"] / avg_s / 1e12
         return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
-                    peak_note="derived: 148 SM x 4 SMSP x 16 FMA/clk x 2 FLOP x 1.965 GHz (FHFMA.BF16 on the FMA pipe)")
+                    peak_note="derived: 148 SM x 128 FP32 FMA/clk x 2 FLOP x 1.965 GHz (full-rate FFMA); the "
+                              "LSTM gather's bound is its critical path, see DESIGN.md")
     # tensor: bf16 measured burst peak (MEASURED_PEAKS.json); TF32 and INT8 measured
     # in this run (cuBLAS 8192^3, measured_tensor_peaks), else the nominal ratios
     peak = pk["bf16_tflops"]
