@@ -426,6 +426,7 @@ struct GatOp {
 // tolerance), while FP64 adds cost nothing on this memory-bound loop; a
 // fast-path batch is pre-summed in fp32 (U = 8 terms).  Row value: 1/|row|
 // (R-GCN per-type mean, reading A24; 0 for a type with no in-edges) or none.
+template <bool kHeavy>
 struct SumF32Op {
     static constexpr int kWin = 1;
     static constexpr int kSlot = 2 * 32 * 4;  // doubles as float pairs
@@ -445,12 +446,11 @@ struct SumF32Op {
     // load in the row flush): the mean's 1/|row|, or for the plain sum 1, or
     // -(slot + 1) for a heavy row (its fp64 copy goes to Sx[slot]).
     __device__ __forceinline__ float row_value(int32_t r, int) const {
-        if (scale) return __ldg(scale + r);
-        if (Sx) {
+        if constexpr (kHeavy) {  // (the gated layer's plain sums: no scale)
             const int32_t hs = __ldg(hslot + r / T);
             return hs >= 0 ? -(float)(hs + 1) : 1.0f;
         }
-        return 1.0f;
+        return scale ? __ldg(scale + r) : 1.0f;
     }
     __device__ __forceinline__ void zero(Acc &c) const {
 #pragma unroll
@@ -483,10 +483,10 @@ struct SumF32Op {
         c.a[3] += (double)v.x.w;
     }
     __device__ __forceinline__ void finish(int32_t r, const Acc &c, float rs, int lane, const float *) const {
-        const double d = rs < 0.0f ? 1.0 : (double)rs;
+        const double d = (kHeavy && rs < 0.0f) ? 1.0 : (double)rs;
         reinterpret_cast<float4 *>(S + (int64_t)r * 128)[lane] =
             make_float4((float)(c.a[0] * d), (float)(c.a[1] * d), (float)(c.a[2] * d), (float)(c.a[3] * d));
-        if (rs < 0.0f) {  // heavy row: also the fp64 sums
+        if (kHeavy && rs < 0.0f) {  // heavy row: also the fp64 sums
             const int64_t hs = (int64_t)(-rs) - 1;
             double2 *x = reinterpret_cast<double2 *>(Sx + (hs * T + r % T) * 128) + lane * 2;
             x[0] = make_double2(c.a[0], c.a[1]);
@@ -1063,11 +1063,12 @@ cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, f
                                  AggWorkspace ws, cudaStream_t st) {
     if (f != 128) return cudaErrorInvalidValue;
     const GraphView gv = g.trow_ptr ? view_typed(g) : view(g);  // no edge types: T = 1
-    SumF32Op op{H, mean ? (g.trow_ptr ? g.tinv_deg : g.inv_deg) : nullptr, S, g.heavy_slot, Sx,
-                g.trow_ptr ? g.num_etypes : 1};
     // U = 4 at 64 registers: measured 3-4% faster than U = 8 (C4, C6), and
     // U = 8 needs more registers (spills at 64, 15% slower at 3 blocks/SM)
-    return run<4, 4>(gv, op, ws, st);
+    const float *scale = mean ? (g.trow_ptr ? g.tinv_deg : g.inv_deg) : nullptr;
+    const int32_t T = g.trow_ptr ? g.num_etypes : 1;
+    if (Sx) return run<4, 4>(gv, SumF32Op<true>{H, scale, S, g.heavy_slot, Sx, T}, ws, st);
+    return run<4, 4>(gv, SumF32Op<false>{H, scale, S, nullptr, nullptr, T}, ws, st);
 }
 
 cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t f, bool relu, bool max, float *m,
