@@ -523,6 +523,8 @@ def run_saga(args, cfg):
     stream = torch.cuda.current_stream()
     ext = {} if args.eager else {"external": True}
 
+    trace_box = []  # region 2's launch spans (saga_profile_trace)
+
     def region(profiled, only=None, do_flush=True):
         starts = [torch.cuda.Event(enable_timing=True, **ext) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True, **ext) for _ in range(args.steps)]
@@ -552,6 +554,8 @@ def run_saga(args, cfg):
             timed_steps()
         torch.cuda.synchronize()
         prof = saga.saga_profile_read()
+        if profiled and not only:
+            trace_box[:] = saga.saga_profile_trace()
         saga.saga_profile_enable(False)
         saga.saga_profile_filter(None)
         if ws > 1:
@@ -617,7 +621,7 @@ def run_saga(args, cfg):
                      "mean_ms": sum(warm_ms) / len(warm_ms), "median_ms": statistics.median(warm_ms),
                      "min_ms": min(warm_ms),
                      "value": job_value(upd_step, args.steps, ws, max_over_ranks(sum(warm_ms), dev))},
-                 "graph_view": gs, "peaks": pk,
+                 "graph_view": gs, "peaks": pk, "stages": stage_breakdown(cfg, trace_box, args.steps),
                  "ms_per_step_profiled": tot_prof_ms / args.steps,
                  "launch": "eager" if args.eager else "CUDA graph: the K timed steps captured once, replayed once"})
     res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -626,8 +630,65 @@ def run_saga(args, cfg):
            "data": "synthetic (seeded counter-based generator, workloads/)", "config": conf,
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
     emit(res, rank)
+    if args.timeline and rank == 0:
+        write_timeline(args.timeline, cfg, trace_box)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+# SAGA-NN stage of each bracketed launch (SURVEY 8(a)
+# S2-S5): the B200 analogue of the paper's per-stage breakdown (Fig. 5,
+# lines 289, 309-310).  Fused kernels carry every stage they run.
+STAGES = {
+    "gcn_f32_fused": "S3+S4+S5 Scatter/Gather/ApplyVertex (fused)",
+    "agg_gcn_bf16": "S3+S4 Scatter/Gather (+S5 epilogue)",
+    "agg_mean_bf16": "S3+S4 Scatter/Gather",
+    "agg_typed_f32": "S3+S4 Scatter/Gather",
+    "agg_typed_mean_f32": "S3+S4 Scatter/Gather",
+    "gat_edge": "S3+S4 Scatter/ApplyEdge/Gather (+S5 epilogue)",
+    "agg_edge_mlp_f32": "S3+S4 Scatter/ApplyEdge/Gather",
+    "gemm_bf16_tc_gat": "S2 pre-projection + ApplyEdge scores",
+    "ggnn_edge_i8x": "S2 pre-projection (edge MLP)",
+    "ggnn_heavy_b_f64": "S2 pre-projection (edge MLP, heavy rows)",
+    "ggnn_split_weights": "S5 ApplyVertex (weight split)",
+    "lstm_input_gemm": "S2 pre-projection (LSTM input)",
+    "lstm_gather": "S4 Gather (LSTM)",
+    "gated_apply_tf32x3": "S5 ApplyVertex",
+    "rgcn_apply_tf32x3": "S5 ApplyVertex",
+    "ggnn_gru_tf32x3": "S5 ApplyVertex",
+    "gru_heavy_f64": "S5 ApplyVertex (heavy rows)",
+    "sage_fused_tc": "S3+S4+S5 Scatter/Gather/ApplyVertex (fused)",
+}
+
+
+def stage_of(cfg, label):
+    if label == "gemm_bf16_tc":  # GCN: the weight moved ahead of Scatter; SAGE/LSTM: ApplyVertex
+        return "S2 pre-projection" if cfg.model == "gcn" else "S5 ApplyVertex"
+    return STAGES.get(label, "other")
+
+
+def stage_breakdown(cfg, trace, steps):
+    """{stage: {"ms_per_step", "share"}} from region 2's spans (serialised
+    launches: the stage times are upper bounds, their shares the breakdown)."""
+    if not trace:
+        return None
+    per = {}
+    for label, t0, t1 in trace:
+        st = stage_of(cfg, label)
+        per[st] = per.get(st, 0.0) + (t1 - t0)
+    tot = sum(per.values())
+    return {k: {"ms_per_step": v / steps, "share": v / tot if tot > 0 else None} for k, v in per.items()}
+
+
+def write_timeline(path, cfg, trace):
+    """Chrome trace-event JSON: one complete event per launch (ts/dur in us)."""
+    ev = [{"name": label, "cat": stage_of(cfg, label), "ph": "X", "ts": t0 * 1e3, "dur": (t1 - t0) * 1e3,
+           "pid": cfg.name, "tid": stage_of(cfg, label), "args": {"stage": stage_of(cfg, label)}}
+          for label, t0, t1 in trace]
+    with open(path, "w") as f:
+        json.dump({"traceEvents": ev, "displayTimeUnit": "ms",
+                   "otherData": {"workload": cfg.name, "source": "bench.py region 2: CUDA event pair per launch "
+                                 "(saga_profile_trace), serialised launches"}}, f)
 
 
 def run_e2e(args, cfg, saga, H, d, dev, ws):
@@ -719,6 +780,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="diagnostic: no per-kernel event pairs in the timed graph (no roofline)")
+    ap.add_argument("--timeline", default=None,
+                    help="write region 2's per-launch spans, tagged with their SAGA stage, as a Chrome trace "
+                         "(chrome://tracing / Perfetto) to this path")
     ap.add_argument("--traffic", type=float, default=None,
                     help="override: ncu dram bytes per launch of the dominant kernel "
                          "(default: profiles/ncu_traffic.json)")

@@ -241,6 +241,14 @@ SAGA_API saga_status saga_profile_enable(int enable);
 SAGA_API saga_status saga_profile_filter(const char *label);
 SAGA_API int32_t saga_profile_count(void);
 SAGA_API saga_status saga_profile_get(int32_t index, const char **name, int64_t *launches, double *total_ms);
+/* Stage timeline (the B200 analogue of the paper's per-stage breakdown,
+ * PAPER.md Fig. 5 / lines 289, 309-310): every bracketed launch since the
+ * last saga_profile_enable, in launch order, as [start_ms, end_ms) measured
+ * by the same event pairs from the first bracket's start event.  `name` is the
+ * library's label (owned by the library, valid until unload).  Synchronises
+ * the pending events; SAGA_EINVAL for an index outside [0, count). */
+SAGA_API int32_t saga_profile_trace_count(void);
+SAGA_API saga_status saga_profile_trace_get(int32_t index, const char **name, double *start_ms, double *end_ms);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 SAGA_API const char *saga_last_error(void);

@@ -32,7 +32,8 @@ MODELS = {"gcn": SAGA_GCN, "sage": SAGA_SAGE, "gat": SAGA_GAT, "gated": SAGA_GAT
 # Every symbol include/saga.h declares (checked by tests/test_abi.py).
 EXPORTS = ["saga_abi_version", "saga_graph_build", "saga_graph_info", "saga_graph_copy_csr",
            "saga_layer_workspace_bytes", "saga_layer", "saga_free", "saga_last_error",
-           "saga_profile_enable", "saga_profile_filter", "saga_profile_count", "saga_profile_get"]
+           "saga_profile_enable", "saga_profile_filter", "saga_profile_count", "saga_profile_get",
+           "saga_profile_trace_count", "saga_profile_trace_get"]
 
 
 class SagaError(RuntimeError):
@@ -91,6 +92,11 @@ def _load():
     L.saga_profile_get.restype = ctypes.c_int
     L.saga_profile_get.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64),
                                    ctypes.POINTER(ctypes.c_double)]
+    L.saga_profile_trace_count.restype = ctypes.c_int32
+    L.saga_profile_trace_count.argtypes = []
+    L.saga_profile_trace_get.restype = ctypes.c_int
+    L.saga_profile_trace_get.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
     return L
 
 
@@ -118,6 +124,17 @@ def saga_profile_read() -> dict:
         name, n, ms = ctypes.c_char_p(), ctypes.c_int64(), ctypes.c_double()
         _check(_lib.saga_profile_get(i, ctypes.byref(name), ctypes.byref(n), ctypes.byref(ms)))
         out[name.value.decode()] = (n.value, ms.value)
+    return out
+
+
+def saga_profile_trace() -> list:
+    """[(label, start ms, end ms)] of every bracketed launch since the last
+    enable, in launch order (times from the first bracket's start)."""
+    out = []
+    for i in range(_lib.saga_profile_trace_count()):
+        name, t0, t1 = ctypes.c_char_p(), ctypes.c_double(), ctypes.c_double()
+        _check(_lib.saga_profile_trace_get(i, ctypes.byref(name), ctypes.byref(t0), ctypes.byref(t1)))
+        out.append((name.value.decode(), t0.value, t1.value))
     return out
 
 

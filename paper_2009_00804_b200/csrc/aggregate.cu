@@ -220,7 +220,11 @@ struct GcnF32FusedOp {
         if (f_out <= 16) {
             // narrow outputs (C1: 64 -> 16): lane = (k half, column); each half
             // runs its own dependent FMA chains over half the inputs (one per
-            // NPL slot), folded by one shuffle -- a quarter of the chain length
+            // NPL slot), folded by one shuffle -- a quarter of the chain length.
+            // The halves' W rows are f_in f_out / 2 floats apart (0 mod 32 at
+            // f_out = 16): the upper half walks its NPL slots in reverse, so
+            // the two addresses of one load differ by an odd multiple of 16
+            // floats and fall in disjoint banks (NPL >= 2).
             const int j = lane & 15, kh = lane >> 4, nk = f_in / NPL;
             float o[NPL];
 #pragma unroll
@@ -228,8 +232,10 @@ struct GcnF32FusedOp {
             for (int kl = kh * (nk / 2); kl < (kh + 1) * (nk / 2); ++kl) {
 #pragma unroll
                 for (int i = 0; i < NPL; ++i) {
-                    const float hk = __shfl_sync(kFull, h[i], kl);
-                    if (j < f_out) o[i] = fmaf(hk, Ws[(kl * NPL + i) * f_out + j], o[i]);
+                    const int ii = kh ? NPL - 1 - i : i;
+                    // (lane kl serves the half that reads kl: lanes >= nk / 2 the upper one)
+                    const float hk = __shfl_sync(kFull, lane >= nk / 2 ? h[NPL - 1 - i] : h[i], kl);
+                    if (j < f_out) o[i] = fmaf(hk, Ws[(kl * NPL + ii) * f_out + j], o[i]);
                 }
             }
             float acc = 0.0f;
@@ -717,7 +723,7 @@ struct DenseWarp {
 // kRmap: the view maps its rows to output rows (the aggregation view); a
 // compile-time switch -- as a runtime one it cost the GAT kernel 25%.
 template <int U, int kMinB, typename Op, bool kRmap>
-__global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, const Op op, const AggWorkspace ws,
+__global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, const __grid_constant__ Op op, const AggWorkspace ws,
                                                           const float *Wg, const int32_t w_elems) {
     constexpr int kWin = Op::kWin;
     constexpr int kWinD = kWin ? kWin : 1;

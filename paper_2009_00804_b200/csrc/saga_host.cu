@@ -59,6 +59,11 @@ struct Prof {
     std::vector<double> ms;
     std::vector<ProfRec> pending;
     std::vector<cudaEvent_t> pool;
+    // timeline: every bracketed launch in launch order, start and end in ms
+    // from the first bracket opened since saga_profile_enable (origin)
+    cudaEvent_t origin = nullptr;
+    struct Span { int name; double t0, t1; };
+    std::vector<Span> trace;
     cudaEvent_t get() {
         if (!pool.empty()) {
             cudaEvent_t e = pool.back();
@@ -84,7 +89,10 @@ struct Prof {
             cudaEventElapsedTime(&t, r.a, r.b);
             ms[r.name] += t;
             launches[r.name] += 1;
-            pool.push_back(r.a);
+            float t0 = 0.f;
+            cudaEventElapsedTime(&t0, origin, r.a);
+            trace.push_back(Span{r.name, (double)t0, (double)t0 + t});
+            if (r.a != origin) pool.push_back(r.a);
             pool.push_back(r.b);
         }
         pending.clear();
@@ -105,6 +113,7 @@ struct ProfScope {
         r.name = g_prof.id(name);
         r.a = g_prof.get();
         r.b = g_prof.get();
+        if (!g_prof.origin) g_prof.origin = r.a;
         // under stream capture the pair must be event-record NODES of the graph
         // (external); outside capture the flag is an error
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -376,6 +385,9 @@ saga_status saga_profile_enable(int enable) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.drain();
     g_prof.on = enable != 0;
+    if (g_prof.origin) g_prof.pool.push_back(g_prof.origin);
+    g_prof.origin = nullptr;
+    g_prof.trace.clear();
     std::fill(g_prof.launches.begin(), g_prof.launches.end(), 0);
     std::fill(g_prof.ms.begin(), g_prof.ms.end(), 0.0);
     return SAGA_OK;
@@ -399,6 +411,23 @@ saga_status saga_profile_get(int32_t index, const char **name, int64_t *launches
     if (name) *name = g_prof.names[index].c_str();
     if (launches) *launches = g_prof.launches[index];
     if (total_ms) *total_ms = g_prof.ms[index];
+    return SAGA_OK;
+}
+
+int32_t saga_profile_trace_count(void) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.drain();
+    return (int32_t)g_prof.trace.size();
+}
+
+saga_status saga_profile_trace_get(int32_t index, const char **name, double *start_ms, double *end_ms) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.drain();
+    if (index < 0 || index >= (int32_t)g_prof.trace.size()) return fail(SAGA_EINVAL, "trace index out of range");
+    const Prof::Span &sp = g_prof.trace[index];
+    if (name) *name = g_prof.names[sp.name].c_str();
+    if (start_ms) *start_ms = sp.t0;
+    if (end_ms) *end_ms = sp.t1;
     return SAGA_OK;
 }
 

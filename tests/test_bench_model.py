@@ -123,3 +123,27 @@ def test_cpu_baseline_sample_grows_to_the_time_target(bench):
     assert f"{c.n} random destination rows" in cpu["sample"] and " runs" in cpu["sample"]
     none = bench.sized_cpu_baseline(c, d, og, oracle, ref_edges=64, ref_seconds=0)
     assert " runs" not in none["sample"]
+
+
+@pytest.mark.parametrize("cfg", sorted(W.CONFIGS))
+def test_every_model_kernel_has_a_stage(bench, cfg):
+    """The stage timeline tags every modelled launch with its SAGA stage."""
+    c = W.CONFIGS[cfg]
+    for k in bench.algorithmic(c):
+        assert bench.stage_of(c, k) != "other", k
+
+
+def test_stage_breakdown_and_timeline(bench, tmp_path):
+    import json
+    c = W.CONFIGS["C5"]
+    trace = [("gemm_bf16_tc", 0.0, 0.7), ("agg_gcn_bf16", 0.7, 4.2), ("gemm_bf16_tc", 5.0, 5.8),
+             ("agg_gcn_bf16", 5.8, 9.0)]
+    st = bench.stage_breakdown(c, trace, 2)
+    assert st["S2 pre-projection"]["ms_per_step"] == pytest.approx(0.75)
+    assert st["S3+S4 Scatter/Gather (+S5 epilogue)"]["ms_per_step"] == pytest.approx(3.35)
+    assert sum(v["share"] for v in st.values()) == pytest.approx(1.0)
+    assert bench.stage_breakdown(c, [], 2) is None
+    p = tmp_path / "t.json"
+    bench.write_timeline(str(p), c, trace)
+    ev = json.load(open(p))["traceEvents"]
+    assert len(ev) == 4 and ev[1]["ts"] == pytest.approx(700.0) and ev[1]["dur"] == pytest.approx(3500.0)
