@@ -226,7 +226,7 @@ def algorithmic(cfg, gs=None):
                                      "peak": "tensor_tf32x3"}
         if gs:  # heavy rows: fp64 message GEMM + GRU from the fp64 sums (gru_f64.cu)
             nh = gs["n_heavy"]
-            out["gru_heavy_f64"] = {"bytes": nh * (T * f * 8 + f * 4 * 2 + 4) + (T + 6) * f * f * (4 + 8),
+            out["gru_heavy_f64"] = {"bytes": nh * (T * f * 8 + f * 4 * 2 + 4) + (T + 6) * f * f * 8,
                                     "flops": 2 * nh * (T * f * f + 6 * f * f), "peak": "fp64_pipe"}
     elif cfg.model == "sage_lstm":
         f, fo = cfg.dims
@@ -260,7 +260,7 @@ def algorithmic(cfg, gs=None):
         out["ggnn_gru_tf32x3"] = {"bytes": n * f * 4 * 4, "flops": 2 * n * 6 * f * f, "peak": "tensor_tf32x3"}
         if gs:  # heavy rows in fp64: their B before the gather, the GRU after it (gru_f64.cu)
             nh = gs["n_heavy"]
-            out["ggnn_heavy_b_f64"] = {"bytes": nh * (f * 4 + f * 8) + 7 * f * f * (4 + 8), "flops": 2 * nh * f * f,
+            out["ggnn_heavy_b_f64"] = {"bytes": nh * (f * 4 + f * 8) + f * f * 8, "flops": 2 * nh * f * f,
                                        "peak": "fp64_pipe"}
             out["gru_heavy_f64"] = {"bytes": nh * (f * 8 + f * 4 * 2 + 4) + 6 * f * f * 8,
                                     "flops": 2 * nh * 6 * f * f, "peak": "fp64_pipe"}
@@ -285,7 +285,8 @@ def roofline_of(name, spec, avg_s, pk, traffic):
         peak = FP64_PIPE_TFLOPS
         ach = spec["flops"] / avg_s / 1e12
         return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
-                    peak_note="derived: 148 SM x 64 DFMA/clk x 2 FLOP x 1.965 GHz (CUDA-core FP64)")
+                    peak_note="derived: 148 SM x 64 fp64 FMA/clk x 2 FLOP x 1.965 GHz (the DMMA tensor path and "
+                              "DFMA share it: ncu sm__ops_path_tensor_src_fp64 peak 128 ops/clk/SM)")
     if spec["peak"] == "fma_pipe":
         # the full-rate FP32 FMA pipe: 148 SMs x 128 FMA/clk x 2 FLOP x 1.965 GHz = 74.4 TFLOP/s.
         # (Round 1 held the LSTM gather to the half-rate FHFMA.BF16 instruction it uses, 37.2 --

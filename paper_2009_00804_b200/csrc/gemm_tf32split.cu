@@ -328,8 +328,12 @@ __device__ __forceinline__ float gru_bt(int f, const float *__restrict__ W_ih, c
 
 __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, const float *__restrict__ W_ih,
                                 const float *__restrict__ W_hh, float *bm_hi, float *bm_lo, float *bg_hi,
-                                float *bg_lo) {
+                                float *bg_lo, double *w64) {
     griddep_wait();
+    if (w64)  // the heavy rows' fp64 weights (gru_f64.cu)
+        for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < heavy_weights_f64_count(T, false);
+             i += gridDim.x * blockDim.x)
+            heavy_weights_f64_item(i, T, W_type, W_ih, W_hh, nullptr, w64);
     const int nm = f * T * f, ng = 4 * f * 2 * f;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nm + ng; i += gridDim.x * blockDim.x) {
         float x;
@@ -354,8 +358,12 @@ __global__ void k_split_weights(int f, int T, const float *__restrict__ W_type, 
 // W_b = W_e[f:2f] columns), its bias vector [0 | b_e], and the GRU B^T.
 __global__ void k_split_ggnn(int f, const float *__restrict__ W_e, const float *__restrict__ b_e,
                              const float *__restrict__ W_ih, const float *__restrict__ W_hh, float *be_hi,
-                             float *be_lo, float *bias2, float *bg_hi, float *bg_lo) {
+                             float *be_lo, float *bias2, float *bg_hi, float *bg_lo, double *w64) {
     griddep_wait();
+    if (w64)  // the heavy rows' fp64 weights (gru_f64.cu): W_ih, W_hh, W_b = W_e rows f .. 2f-1
+        for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < heavy_weights_f64_count(0, true);
+             i += gridDim.x * blockDim.x)
+            heavy_weights_f64_item(i, 0, nullptr, W_ih, W_hh, W_e + (int64_t)f * f, w64);
     const int ne = 2 * f * f, ng = 4 * f * 2 * f;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ne + ng + 2 * f; i += gridDim.x * blockDim.x) {
         if (i >= ne + ng) {
@@ -475,8 +483,8 @@ size_t gated_tc_workspace_floats(int32_t f, int32_t T) { return (size_t)2 * f * 
 
 cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
-                                  const float *b_hh, float *m_ws, float *wsplit, float *out, cudaStream_t st,
-                                  const char **why) {
+                                  const float *b_hh, float *m_ws, float *wsplit, double *w64, float *out,
+                                  cudaStream_t st, const char **why) {
     if (M == 0) return cudaSuccess;
     if (f != 128 || T < 1 || T > 4) {
         *why = "tensor-core gated path needs f = 128, 1 <= T <= 4";
@@ -484,7 +492,8 @@ cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *
     }
     float *bm_hi = wsplit, *bm_lo = bm_hi + (size_t)f * T * f;
     float *bg_hi = bm_lo + (size_t)f * T * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
-    cudaError_t e = launch<false>(k_split_weights, 256, 256, 0, st, f, T, W_type, W_ih, W_hh, bm_hi, bm_lo, bg_hi, bg_lo);
+    cudaError_t e = launch<false>(k_split_weights, 256, 256, 0, st, f, T, W_type, W_ih, W_hh, bm_hi, bm_lo, bg_hi, bg_lo,
+                                  w64);
     if (e) return e;
     CUtensorMap aS, aM, aH, bmh, bml, bgh, bgl;
     if (!make_map_f32(&aS, S, M, (int64_t)T * f, (int64_t)T * f, kBM) || !make_map_f32(&aM, m_ws, M, f, f, kBM) ||
@@ -506,10 +515,11 @@ size_t ggnn_tc_workspace_floats(int32_t f) { return (size_t)2 * 2 * f * f + 2 * 
 // GGNN (NEXT-4): the GRU's split B^T (the edge-MLP projection AB runs on the
 // int8-sliced exact-accumulation GEMM, gemm_i8x.cu).
 cudaError_t launch_ggnn_split_weights(int32_t f, const float *W_e, const float *b_e, const float *W_ih,
-                                      const float *W_hh, float *wsplit, cudaStream_t st) {
+                                      const float *W_hh, float *wsplit, double *w64, cudaStream_t st) {
     float *be_hi = wsplit, *be_lo = be_hi + (size_t)2 * f * f, *bias2 = be_lo + (size_t)2 * f * f;
     float *bg_hi = bias2 + 2 * f, *bg_lo = bg_hi + (size_t)4 * f * 2 * f;
-    return launch<false>(k_split_ggnn, 256, 256, 0, st, f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo);
+    return launch<false>(k_split_ggnn, 256, 256, 0, st, f, W_e, b_e, W_ih, W_hh, be_hi, be_lo, bias2, bg_hi, bg_lo,
+                         w64);
 }
 
 cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float *H, const float *b_ih,

@@ -32,17 +32,20 @@
 // that wrote them), so the result is deterministic.
 //
 // Cost: per heavy row (T f + 6 f) f fp64 FMAs (164K at C4) -- 834 rows at
-// C4/C8 (0.64% of the vertices, 39% of the edges).  A CTA takes kR = 8 rows
-// and thread j owns column j of all 8 rows (8 accumulators per output
-// matrix, 48 in the gate phase), so each weight element read from shared
-// memory feeds 8 FMAs and the row operands are broadcasts.  The weights
-// (converted to fp64 once per call by k_weights_f64) stream through a
-// two-slot shared-memory ring of 48 KB chunks filled by bulk copies
-// (cp.async.bulk, one thread) while the previous chunk is consumed.
-// Measured on the way (C4): weights read from L2 per FMA were latency-bound
-// (60 us), fp32 weights converted per use bound the XU pipe (F2F, 66 us),
-// and a (row, column-quad) thread mapping was bound by shared-memory
-// wavefronts (8 x re-reads of every weight, 2-way conflicts: 107 us).
+// C4/C8 (0.64% of the vertices, 39% of the edges).  A CTA takes kR = 8 rows,
+// the M of the fp64 tensor-core MMA (mma.sync m8n8k4 f64, DMMA): warp w owns
+// output columns [16 w, 16 w + 16) as two 8-column n-tiles, so one A fragment
+// (8 rows x 4 k, one double per lane) feeds two MMAs and each weight double
+// read from shared memory feeds 8 FMAs inside the MMA.  The operands sit in
+// shared memory in fragment order -- A as [k/4][row][k%4], the weights as
+// [k/4][n/8][n%8][k%4] (permuted once per call by k_weights_f64) -- so every
+// fragment load is one conflict-free 256-byte LDS.64.  The weights stream
+// through a two-slot ring of 48 KB chunks filled by bulk copies (one thread)
+// while the previous chunk is consumed.
+// Measured on the way (C4): the FFMA form with thread = (4 rows, column) was
+// bound by shared-memory wavefronts (one LDS per DFMA: 48 us); before it,
+// weights read from L2 per FMA (60 us), fp32 weights converted per use (F2F on
+// the XU pipe, 66 us) and a (row, column-quad) mapping (107 us).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -54,9 +57,9 @@ namespace saga {
 namespace {
 
 constexpr int kF = 128;            // hidden width (in = out = 128, checked by the host)
-constexpr int kR = 8;              // rows per CTA batch
-constexpr int kRT = 4;             // rows per thread: thread = (row group of kRT rows, column)
-constexpr int kThreads = kF * (kR / kRT);
+constexpr int kR = 8;              // rows per CTA batch = the DMMA's M
+constexpr int kThreads = 256;      // 8 warps x 16 output columns
+constexpr int kNT = 2;             // 8-column n-tiles per warp
 constexpr int kSlot = 48 * 1024;   // ring slot (bytes): fp64 weights
 constexpr int kChunkG = 8;         // gate phase: K-rows per chunk (x 6 matrices of [kF][kF] fp64)
 constexpr int kChunkM = 32;        // message / B phase: K-rows per chunk of one [K][kF] fp64 matrix
@@ -65,52 +68,88 @@ struct alignas(16) Ring {
     uint64_t full[2];
 };
 
-// acc[r] += sum_k x[r0 + r][k] W[k][j] for kRT rows: x smem fp64 [kR][ldx], W a
-// [K][kF] fp64 matrix streamed in chunks of kChunkM rows.  The ring's chunk
-// counter `cc` continues across calls (slot = cc & 1, parity = (cc >> 1) & 1).
-__device__ __forceinline__ void stream_gemm(double (&acc)[kRT], const double *x, int ldx, const double *W, int K,
-                                            double *slots, Ring &ring, uint32_t &cc, int r0, int j) {
-    const int nch = K / kChunkM;
-    auto issue = [&](int c, uint32_t seq) {
+// D (8 x 8) += A (8 x 4) . B (4 x 8), fp64; per lane: a = A[lane / 4][lane % 4],
+// b = B[lane % 4][lane / 4], d = D[lane / 4][2 (lane % 4) + {0, 1}]
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// fragment-order position of element (r, k) of an [kR][K] A operand
+__device__ __forceinline__ int afrag(int r, int k) { return (k >> 2) * 32 + r * 4 + (k & 3); }
+
+// The weight chunks of a CTA's whole run form one sequence through the
+// two-slot ring: per batch, the message (or B) GEMM's chunks of kChunkM K-rows
+// (n1 of them, 0 for the GGNN GRU), then the gate phase's chunks of kChunkG
+// K-rows of all six gate matrices (n2).  Thread 0 issues chunk s + 2 as soon
+// as chunk s is consumed -- across phases and batches -- and the first two
+// right after the grid dependency, before the batch's operand loads.
+struct Feed {
+    Ring *ring;
+    double *slots;
+    const double *W1;            // [K1][kF] message / B weights (fragment order)
+    const double *W_ih, *W_hh;   // gate weights, [3][kF][kF] each (fragment order)
+    int n1, n2;                  // chunks per batch of each phase
+    uint32_t total;              // chunks of the CTA's run
+    __device__ void issue(uint32_t seq) const {
+        if (seq >= total) return;
         double *dst = slots + (seq & 1) * (kSlot / 8);
-        ptx::mbar_arrive_expect_tx(&ring.full[seq & 1], kChunkM * kF * 8);
-        ptx::bulk_g2s(dst, W + (int64_t)c * kChunkM * kF, kChunkM * kF * 8, &ring.full[seq & 1]);
-    };
-    if (threadIdx.x == 0) {
-        issue(0, cc);
-        if (nch > 1) issue(1, cc + 1);
+        const int local = (int)(seq % (uint32_t)(n1 + n2));
+        uint64_t *bar = &ring->full[seq & 1];
+        if (local < n1) {
+            ptx::mbar_arrive_expect_tx(bar, kChunkM * kF * 8);
+            ptx::bulk_g2s(dst, W1 + (int64_t)local * kChunkM * kF, kChunkM * kF * 8, bar);
+            return;
+        }
+        const int c = local - n1;
+        ptx::mbar_arrive_expect_tx(bar, 6 * kChunkG * kF * 8);
+        for (int mat = 0; mat < 6; ++mat)
+            ptx::bulk_g2s(dst + mat * kChunkG * kF, (mat < 3 ? W_ih : W_hh) + ((int64_t)(mat % 3) * kF + c * kChunkG) * kF,
+                          kChunkG * kF * 8, bar);
     }
+    // wait for chunk seq; returns its slot
+    __device__ const double *wait(uint32_t seq) const {
+        ptx::mbar_wait(&ring->full[seq & 1], (seq >> 1) & 1);
+        return slots + (seq & 1) * (kSlot / 8);
+    }
+    // every thread is done with chunk seq: refill its slot
+    __device__ void release(uint32_t seq) const {
+        __syncthreads();
+        if (threadIdx.x == 0) issue(seq + 2);
+    }
+};
+
+// acc[t] += x . W1 over K for this warp's n-tiles: x in A-fragment order, the
+// [K][kF] weights arriving through the feed in chunks of kChunkM K-rows.  Two
+// accumulator sets (even / odd k-steps) keep four independent MMA chains per
+// warp.
+__device__ __forceinline__ void stream_mma(double (&acc)[kNT][2], const double *x, int K, const Feed &fd,
+                                           uint32_t &cc, int nt0, int lane) {
+    const int nch = K / kChunkM;
+    double odd[kNT][2] = {};
     for (int c = 0; c < nch; ++c, ++cc) {
-        ptx::mbar_wait(&ring.full[cc & 1], (cc >> 1) & 1);
-        const double *w = slots + (cc & 1) * (kSlot / 8);
-#pragma unroll 2
-        for (int k = 0; k < kChunkM; k += 2) {
-            const double w0 = w[k * kF + j], w1 = w[(k + 1) * kF + j];
+        const double *w = fd.wait(cc);
+        const double *xa = x + c * (kChunkM / 4) * 32 + lane;
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                const double2 xv = *reinterpret_cast<const double2 *>(x + (r0 + r) * ldx + c * kChunkM + k);
-                acc[r] = fma(xv.x, w0, acc[r]);
-                acc[r] = fma(xv.y, w1, acc[r]);
+        for (int kb = 0; kb < kChunkM / 4; kb += 2) {
+            const double a0 = xa[kb * 32], a1 = xa[(kb + 1) * 32];
+#pragma unroll
+            for (int t = 0; t < kNT; ++t) {
+                dmma(acc[t], a0, w[(kb * 16 + nt0 + t) * 32 + lane]);
+                dmma(odd[t], a1, w[((kb + 1) * 16 + nt0 + t) * 32 + lane]);
             }
         }
-        __syncthreads();  // slot consumed by every thread
-        if (threadIdx.x == 0 && c + 2 < nch) issue(c + 2, cc + 2);
+        fd.release(cc);
+    }
+#pragma unroll
+    for (int t = 0; t < kNT; ++t) {
+        acc[t][0] += odd[t][0];
+        acc[t][1] += odd[t][1];
     }
 }
 
-// fp64 copies of the weights the heavy kernels stream: [W_type (T kF kF) | W_ih (3 kF kF) | W_hh | W_b (kF kF)]
-__global__ void k_weights_f64(int32_t nt, const float *__restrict__ W_type, const float *__restrict__ W_ih,
-                              const float *__restrict__ W_hh, const float *__restrict__ W_b, double *__restrict__ out) {
-    griddep_wait();  // before this grid's first global write
-    const int64_t a = (int64_t)nt * kF * kF, g = (int64_t)3 * kF * kF, b = W_b ? (int64_t)kF * kF : 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a + 2 * g + b;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float x = i < a ? W_type[i] : i < a + g ? W_ih[i - a] : i < a + 2 * g ? W_hh[i - a - g] : W_b[i - a - 2 * g];
-        out[i] = (double)x;
-    }
-}
-
-// smem: ring 2 x kSlot | a[kR][T kF] fp64 (gated) | m[kR][kF] fp64 | h[kR][kF] fp64
+// smem: ring 2 x kSlot | a[kR][T kF] (gated) | m[kR][kF] | h[kR][kF], fp64, A-fragment order
 size_t smem_bytes(int T) { return 2 * (size_t)kSlot + sizeof(double) * ((size_t)kR * T * kF + 2 * kR * kF); }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -126,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     double *m = a + (gated ? kR * K : 0);                       // [kR][kF]
     double *h = m + kR * kF;                                    // [kR][kF]
     __shared__ Ring ring;
-    const int j = threadIdx.x % kF, r0 = (threadIdx.x / kF) * kRT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt0 = warp * kNT, r = lane >> 2, c2 = (lane & 3) * 2;  // this lane's D row and column pair
     if (threadIdx.x == 0) {
         ptx::mbar_init(&ring.full[0], 1);
         ptx::mbar_init(&ring.full[1], 1);
@@ -134,84 +174,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     uint32_t cc = 0;  // chunks consumed (ring sequence)
+    const int nb = (nh - (int)blockIdx.x * kR + (int)gridDim.x * kR - 1) / ((int)gridDim.x * kR);  // batches of this CTA
+    const Feed fd{&ring, slots, W_type, W_ih, W_hh, gated ? K / kChunkM : 0, kF / kChunkG,
+                  (uint32_t)nb * (uint32_t)((gated ? K / kChunkM : 0) + kF / kChunkG)};
 
-    griddep_wait();  // Sx / mx and the tensor path's output rows come from the call's earlier kernels
+    griddep_wait();  // Sx / mx, the weights and the tensor path's output rows come from the call's earlier kernels
+    if (threadIdx.x == 0) {
+        fd.issue(0);
+        fd.issue(1);
+    }
     for (int32_t b0 = blockIdx.x * kR; b0 < nh; b0 += gridDim.x * kR) {
         const int nr = min(kR, nh - b0);
-        for (int r = r0; r < r0 + kRT; ++r) {
-            h[r * kF + j] = r < nr ? (double)H[(int64_t)rows[b0 + r] * kF + j] : 0.0;
-            if (!gated) m[r * kF + j] = r < nr ? mx[(int64_t)(b0 + r) * kF + j] : 0.0;
+        for (int i = threadIdx.x; i < kR * kF; i += kThreads) {
+            const int rr = i / kF, j = i % kF;
+            h[afrag(rr, j)] = rr < nr ? (double)H[(int64_t)rows[b0 + rr] * kF + j] : 0.0;
+            if (!gated) m[afrag(rr, j)] = rr < nr ? mx[(int64_t)(b0 + rr) * kF + j] : 0.0;
         }
         if (gated)
-            for (int i = threadIdx.x; i < kR * K; i += kThreads) a[i] = i / K < nr ? Sx[(int64_t)b0 * K + i] : 0.0;
+            for (int i = threadIdx.x; i < kR * K; i += kThreads) {
+                const int rr = i / K, k = i % K;
+                a[afrag(rr, k)] = rr < nr ? Sx[(int64_t)b0 * K + i] : 0.0;
+            }
         __syncthreads();
         if (gated) {
             // m = S . W_type  (W_type [T][kF][kF] = [K][kF])
-            double acc[kRT] = {};
-            stream_gemm(acc, a, K, W_type, K, slots, ring, cc, r0, j);
+            double acc[kNT][2] = {};
+            stream_mma(acc, a, K, fd, cc, nt0, lane);
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) m[(r0 + r) * kF + j] = acc[r];
+            for (int t = 0; t < kNT; ++t) {
+                const int col = (nt0 + t) * 8 + c2;
+                m[afrag(r, col)] = acc[t][0];
+                m[afrag(r, col + 1)] = acc[t][1];
+            }
             __syncthreads();
         }
         // gate pre-activations: gi[g] = m . W_ih[g], gh[g] = h . W_hh[g] (g = r, z, n); the six
-        // matrices stream together in chunks of kChunkG K-rows
-        double gi[3][kRT] = {}, gh[3][kRT] = {};
-        {
-            auto issue = [&](int c, uint32_t seq) {
-                double *dst = slots + (seq & 1) * (kSlot / 8);
-                ptx::mbar_arrive_expect_tx(&ring.full[seq & 1], 6 * kChunkG * kF * 8);
-                for (int mat = 0; mat < 6; ++mat)
-                    ptx::bulk_g2s(dst + mat * kChunkG * kF,
-                                  (mat < 3 ? W_ih : W_hh) + ((int64_t)(mat % 3) * kF + c * kChunkG) * kF,
-                                  kChunkG * kF * 8, &ring.full[seq & 1]);
-            };
-            constexpr int nch = kF / kChunkG;
-            if (threadIdx.x == 0) {
-                issue(0, cc);
-                issue(1, cc + 1);
-            }
-            for (int c = 0; c < nch; ++c, ++cc) {
-                ptx::mbar_wait(&ring.full[cc & 1], (cc >> 1) & 1);
-                const double *w = slots + (cc & 1) * (kSlot / 8);
-                for (int k = 0; k < kChunkG; k += 2) {
-                    double wi[3][2], wh[3][2];
+        // matrices stream together in chunks of kChunkG K-rows, [mat][kChunkG / 4][kF / 8][32] per slot
+        double gi[3][kNT][2] = {}, gh[3][kNT][2] = {};
+        for (int c = 0; c < kF / kChunkG; ++c, ++cc) {
+            const double *w = fd.wait(cc) + lane;
 #pragma unroll
-                    for (int g = 0; g < 3; ++g)
+            for (int kb = 0; kb < kChunkG / 4; ++kb) {
+                const double am = m[(c * (kChunkG / 4) + kb) * 32 + lane];
+                const double ah = h[(c * (kChunkG / 4) + kb) * 32 + lane];
 #pragma unroll
-                        for (int d = 0; d < 2; ++d) {
-                            wi[g][d] = w[(g * kChunkG + k + d) * kF + j];
-                            wh[g][d] = w[((3 + g) * kChunkG + k + d) * kF + j];
-                        }
+                for (int t = 0; t < kNT; ++t)
 #pragma unroll
-                    for (int r = 0; r < kRT; ++r) {
-                        const double2 mv = *reinterpret_cast<const double2 *>(m + (r0 + r) * kF + c * kChunkG + k);
-                        const double2 hv = *reinterpret_cast<const double2 *>(h + (r0 + r) * kF + c * kChunkG + k);
-#pragma unroll
-                        for (int g = 0; g < 3; ++g) {
-                            gi[g][r] = fma(mv.x, wi[g][0], gi[g][r]);
-                            gi[g][r] = fma(mv.y, wi[g][1], gi[g][r]);
-                            gh[g][r] = fma(hv.x, wh[g][0], gh[g][r]);
-                            gh[g][r] = fma(hv.y, wh[g][1], gh[g][r]);
-                        }
+                    for (int g = 0; g < 3; ++g) {
+                        dmma(gi[g][t], am, w[g * kChunkG * kF + (kb * 16 + nt0 + t) * 32]);
+                        dmma(gh[g][t], ah, w[(3 + g) * kChunkG * kF + (kb * 16 + nt0 + t) * 32]);
                     }
-                }
-                __syncthreads();
-                if (threadIdx.x == 0 && c + 2 < nch) issue(c + 2, cc + 2);
             }
+            fd.release(cc);
         }
         // PyTorch GRUCell (reading A15): r = s(gi_r + gh_r), z = s(gi_z + gh_z),
-        // n = tanh(gi_n + r gh_n), h' = (1 - z) n + z h  -- in this thread's registers
-        {
-            const double bir = b_ih[j], biz = b_ih[kF + j], bin = b_ih[2 * kF + j];
-            const double bhr = b_hh[j], bhz = b_hh[kF + j], bhn = b_hh[2 * kF + j];
+        // n = tanh(gi_n + r gh_n), h' = (1 - z) n + z h  -- on this lane's D elements
+        if (r < nr) {
+            float *o = out + (int64_t)rows[b0 + r] * kF;
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                if (r0 + r >= nr) break;
-                const double rg = 1.0 / (1.0 + exp(-(gi[0][r] + bir + gh[0][r] + bhr)));
-                const double zg = 1.0 / (1.0 + exp(-(gi[1][r] + biz + gh[1][r] + bhz)));
-                const double n = tanh(gi[2][r] + bin + rg * (gh[2][r] + bhn));
-                out[(int64_t)rows[b0 + r0 + r] * kF + j] = (float)((1.0 - zg) * n + zg * h[(r0 + r) * kF + j]);
-            }
+            for (int t = 0; t < kNT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = (nt0 + t) * 8 + c2 + e;
+                    const double rg = 1.0 / (1.0 + exp(-(gi[0][t][e] + b_ih[j] + gh[0][t][e] + b_hh[j])));
+                    const double zg = 1.0 / (1.0 + exp(-(gi[1][t][e] + b_ih[kF + j] + gh[1][t][e] + b_hh[kF + j])));
+                    const double n = tanh(gi[2][t][e] + b_ih[2 * kF + j] + rg * (gh[2][t][e] + b_hh[2 * kF + j]));
+                    o[j] = (float)((1.0 - zg) * n + zg * h[afrag(r, j)]);
+                }
         }
         __syncthreads();  // m, h, a are rewritten by the next batch
     }
@@ -224,9 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const double *__restrict__ W_b, const float *__restrict__ b_e, double *__restrict__ Bx) {
     extern __shared__ __align__(16) uint8_t smem[];
     double *slots = reinterpret_cast<double *>(smem);
-    double *hs = reinterpret_cast<double *>(smem + 2 * kSlot);  // [kR][kF]
+    double *hs = reinterpret_cast<double *>(smem + 2 * kSlot);  // [kR][kF], A-fragment order
     __shared__ Ring ring;
-    const int j = threadIdx.x % kF, r0 = (threadIdx.x / kF) * kRT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt0 = warp * kNT, r = lane >> 2, c2 = (lane & 3) * 2;
     if (threadIdx.x == 0) {
         ptx::mbar_init(&ring.full[0], 1);
         ptx::mbar_init(&ring.full[1], 1);
@@ -234,15 +264,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     uint32_t cc = 0;
-    griddep_wait();  // before this grid's first global write
-    const double b = b_e ? (double)b_e[j] : 0.0;
+    const int nb = (nh - (int)blockIdx.x * kR + (int)gridDim.x * kR - 1) / ((int)gridDim.x * kR);
+    const Feed fd{&ring, slots, W_b, nullptr, nullptr, kF / kChunkM, 0, (uint32_t)nb * (uint32_t)(kF / kChunkM)};
+    griddep_wait();  // the weights come from the call's split-weights kernel
+    if (threadIdx.x == 0) {
+        fd.issue(0);
+        fd.issue(1);
+    }
     for (int32_t b0 = blockIdx.x * kR; b0 < nh; b0 += gridDim.x * kR) {
         const int nr = min(kR, nh - b0);
-        for (int r = r0; r < r0 + kRT; ++r) hs[r * kF + j] = r < nr ? (double)H[(int64_t)rows[b0 + r] * kF + j] : 0.0;
+        for (int i = threadIdx.x; i < kR * kF; i += kThreads) {
+            const int rr = i / kF, j = i % kF;
+            hs[afrag(rr, j)] = rr < nr ? (double)H[(int64_t)rows[b0 + rr] * kF + j] : 0.0;
+        }
         __syncthreads();
-        double acc[kRT] = {};
-        stream_gemm(acc, hs, kF, W_b, kF, slots, ring, cc, r0, j);
-        for (int r = 0; r < kRT && r0 + r < nr; ++r) Bx[(int64_t)(b0 + r0 + r) * kF + j] = acc[r] + b;
+        double acc[kNT][2] = {};
+        stream_mma(acc, hs, kF, fd, cc, nt0, lane);
+        if (r < nr)
+#pragma unroll
+            for (int t = 0; t < kNT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = (nt0 + t) * 8 + c2 + e;
+                    Bx[(int64_t)(b0 + r) * kF + j] = acc[t][e] + (b_e ? (double)b_e[j] : 0.0);
+                }
         __syncthreads();
     }
 }
@@ -280,14 +325,6 @@ size_t heavy_workspace_bytes(const GraphDev &g, saga_model kind, int32_t f) {
     if (kind == SAGA_GATED) return sizeof(double) * (nh * T * kF + (T + 6) * ff);
     if (kind == SAGA_GGNN) return sizeof(double) * (2 * nh * kF + 7 * ff);
     return 0;
-}
-
-cudaError_t launch_heavy_weights_f64(const GraphDev &g, const HeavyWs &w, const float *W_type, const float *W_ih,
-                                     const float *W_hh, const float *W_e, cudaStream_t st) {
-    if (g.n_heavy == 0) return cudaSuccess;
-    const float *W_b = W_e ? W_e + (int64_t)kF * kF : nullptr;  // W_e [2f][f]: destination half
-    return launch(k_weights_f64, 2 * kNumSMs, 256, 0, st, (int32_t)(W_type ? w.T : 0), W_type, W_ih, W_hh, W_b,
-                  w.W64);
 }
 
 cudaError_t launch_ggnn_heavy_b(const GraphDev &g, const HeavyWs &w, const float *H, const float *b_e,

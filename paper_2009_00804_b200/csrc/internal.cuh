@@ -180,8 +180,24 @@ struct HeavyWs {
 };
 size_t heavy_workspace_bytes(const GraphDev &g, saga_model kind, int32_t f);
 HeavyWs heavy_ws(const GraphDev &g, saga_model kind, void *base);
-cudaError_t launch_heavy_weights_f64(const GraphDev &g, const HeavyWs &w, const float *W_type, const float *W_ih,
-                                     const float *W_hh, const float *W_e, cudaStream_t st);
+// Element i of the heavy kernels' fp64 weights [W_type (nt f f) | W_ih (3 f f) |
+// W_hh | W_b (f f, if given)], every [K][f] matrix in the fp64 MMA's B-fragment
+// order [k/4][n/8][n%8][k%4] (f = 128).  Written by the call's split-weights
+// kernel (gemm_tf32split.cu) in the same pass as the tf32 hi/lo split; the
+// count is heavy_weights_f64_count.
+__device__ __forceinline__ void heavy_weights_f64_item(int64_t i, int32_t nt, const float *__restrict__ W_type,
+                                                       const float *__restrict__ W_ih, const float *__restrict__ W_hh,
+                                                       const float *__restrict__ W_b, double *__restrict__ out) {
+    constexpr int f = 128;
+    const int64_t a = (int64_t)nt * f * f, g = (int64_t)3 * f * f;
+    const float x = i < a ? W_type[i] : i < a + g ? W_ih[i - a] : i < a + 2 * g ? W_hh[i - a - g] : W_b[i - a - 2 * g];
+    // every matrix starts at a multiple of f f, so permuting the whole buffer
+    // as [rows][f] permutes each matrix in place
+    const int64_t k = i / f;
+    const int n = (int)(i % f);
+    out[((k >> 2) * (f / 8) + (n >> 3)) * 32 + (n & 7) * 4 + (k & 3)] = (double)x;
+}
+__host__ __device__ inline int64_t heavy_weights_f64_count(int32_t nt, bool with_b) { return (int64_t)(nt + 6 + (with_b ? 1 : 0)) * 128 * 128; }
 cudaError_t launch_ggnn_heavy_b(const GraphDev &g, const HeavyWs &w, const float *H, const float *b_e,
                                 cudaStream_t st);
 cudaError_t launch_gru_heavy_f64(const GraphDev &g, const HeavyWs &w, const float *H, const float *b_ih,
@@ -203,8 +219,9 @@ cudaError_t launch_sage_fused(const GraphDev &g, const __nv_bfloat16 *X, int32_t
                               cudaStream_t st, const char **why);
 
 size_t ggnn_tc_workspace_floats(int32_t f);
+// w64 (nullable): also the heavy kernels' fp64 weights (heavy_weights_f64_item)
 cudaError_t launch_ggnn_split_weights(int32_t f, const float *W_e, const float *b_e, const float *W_ih,
-                                      const float *W_hh, float *wsplit, cudaStream_t st);
+                                      const float *W_hh, float *wsplit, double *w64, cudaStream_t st);
 // GGNN edge-MLP projection AB = H . [W_a | W_b] + [0 | b_e] on the int8 tensor
 // cores with exact accumulation (gemm_i8x.cu); ws: ggnn_i8_workspace_bytes(M).
 size_t ggnn_i8_workspace_bytes(int64_t M);
@@ -218,8 +235,8 @@ cudaError_t launch_ggnn_gru_tc(int64_t M, int32_t f, const float *m, const float
 size_t gated_tc_workspace_floats(int32_t f, int32_t T);
 cudaError_t launch_gated_apply_tc(int64_t M, int32_t f, int32_t T, const float *S, const float *H,
                                   const float *W_type, const float *W_ih, const float *W_hh, const float *b_ih,
-                                  const float *b_hh, float *m_ws, float *wsplit, float *out, cudaStream_t st,
-                                  const char **why);
+                                  const float *b_hh, float *m_ws, float *wsplit, double *w64, float *out,
+                                  cudaStream_t st, const char **why);
 
 // GraphSAGE-LSTM Gather (lstm_gather.cu, NEXT-2): h_out[v] = final LSTM state over v's in-edges.
 size_t lstm_workspace_bytes();  // staged W_hh^T + the work-queue head

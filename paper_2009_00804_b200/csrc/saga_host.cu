@@ -591,14 +591,12 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 e = launch_gated_apply_tc(d.n, o.in_dim, d.num_etypes, S, H, w->W_type,
                                           static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
                                           w->b_ih, w->b_hh, m, reinterpret_cast<float *>(i2),
-                                          static_cast<float *>(out->data), st, &why);
+                                          d.n_heavy ? hw.W64 : nullptr, static_cast<float *>(out->data), st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "gated apply: %s (%s)", cudaGetErrorString(e), why);
             if (d.n_heavy) {
-                ProfScope ps_("gru_heavy_f64", st);
-                e = launch_heavy_weights_f64(d, hw, w->W_type, static_cast<const float *>(w->W_ih),
-                                             static_cast<const float *>(w->W_hh), nullptr, st);
-                if (!e) e = launch_gru_heavy_f64(d, hw, H, w->b_ih, w->b_hh, static_cast<float *>(out->data), st);
+                ProfScope ps_("gru_heavy_f64", st);  // (fp64 weights: written by the gated apply's split kernel)
+                e = launch_gru_heavy_f64(d, hw, H, w->b_ih, w->b_hh, static_cast<float *>(out->data), st);
             }
             if (e) return cuda_fail(e, "gated heavy rows");
             return SAGA_OK;
@@ -647,11 +645,12 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             const float *H = static_cast<const float *>(x->data);
             float *AB = reinterpret_cast<float *>(i0), *m = reinterpret_cast<float *>(i1);
             float *wsplit = reinterpret_cast<float *>(i2);
+            const HeavyWs hw = heavy_ws(d, SAGA_GGNN, i3);
             {
-                ProfScope ps_("ggnn_split_weights", st);
+                ProfScope ps_("ggnn_split_weights", st);  // (and the heavy rows' fp64 weights)
                 e = launch_ggnn_split_weights(o.in_dim, static_cast<const float *>(w->W), w->bias,
                                               static_cast<const float *>(w->W_ih), static_cast<const float *>(w->W_hh),
-                                              wsplit, st);
+                                              wsplit, d.n_heavy ? hw.W64 : nullptr, st);
             }
             if (e) return cuda_fail(e, "ggnn split weights");
             {
@@ -663,12 +662,9 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                                          AB, st, &why);
             }
             if (e) return fail(SAGA_ECUDA, "ggnn edge gemm: %s (%s)", cudaGetErrorString(e), why);
-            const HeavyWs hw = heavy_ws(d, SAGA_GGNN, i3);
             if (d.n_heavy) {
                 ProfScope ps_("ggnn_heavy_b_f64", st);
-                e = launch_heavy_weights_f64(d, hw, nullptr, static_cast<const float *>(w->W_ih),
-                                             static_cast<const float *>(w->W_hh), static_cast<const float *>(w->W), st);
-                if (!e) e = launch_ggnn_heavy_b(d, hw, H, w->bias, st);
+                e = launch_ggnn_heavy_b(d, hw, H, w->bias, st);
             }
             if (e) return cuda_fail(e, "ggnn heavy B");
             {
