@@ -58,15 +58,21 @@ namespace {
 
 constexpr int kF = 128;            // hidden width (in = out = 128, checked by the host)
 constexpr int kR = 8;              // rows per CTA batch = the DMMA's M
-constexpr int kThreads = 256;      // 8 warps x 16 output columns
+constexpr int kCompute = 256;      // 8 MMA warps x 16 output columns
+constexpr int kThreads = kCompute + 32;  // + one producer warp (weight chunks)
 constexpr int kNT = 2;             // 8-column n-tiles per warp
 constexpr int kSlot = 48 * 1024;   // ring slot (bytes): fp64 weights
+constexpr int kSlots = 3;          // ring depth
 constexpr int kChunkG = 8;         // gate phase: K-rows per chunk (x 6 matrices of [kF][kF] fp64)
 constexpr int kChunkM = 32;        // message / B phase: K-rows per chunk of one [K][kF] fp64 matrix
 
 struct alignas(16) Ring {
-    uint64_t full[2];
+    uint64_t full[kSlots];   // chunk landed (1 arrival + tx bytes)
+    uint64_t empty[kSlots];  // chunk consumed (one arrival per MMA warp)
 };
+
+// the MMA warps' own barrier (the producer warp never joins)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory"); }
 
 // D (8 x 8) += A (8 x 4) . B (4 x 8), fp64; per lane: a = A[lane / 4][lane % 4],
 // b = B[lane % 4][lane / 4], d = D[lane / 4][2 (lane % 4) + {0, 1}]
@@ -79,12 +85,49 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // fragment-order position of element (r, k) of an [kR][K] A operand
 __device__ __forceinline__ int afrag(int r, int k) { return (k >> 2) * 32 + r * 4 + (k & 3); }
 
+// Operand fills (MMA warps): every global load of a thread is issued before
+// the first shared-memory store -- as a loop with a store per load they were
+// serial round trips (30% of the GGNN GRU's stall samples).
+// dst[afrag(r, j)] = H[rows[b0 + r]][j] (0 past nr rows), [kR][kF]
+__device__ __forceinline__ void fill_rows_f32(double *dst, const float *__restrict__ H, const int32_t *__restrict__ rows,
+                                              int32_t b0, int nr) {
+    constexpr int kPer = kR * kF / kCompute;
+    float v[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = threadIdx.x + q * kCompute, rr = i / kF;
+        v[q] = rr < nr ? __ldg(H + (int64_t)__ldg(rows + b0 + rr) * kF + i % kF) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = threadIdx.x + q * kCompute;
+        dst[afrag(i / kF, i % kF)] = (double)v[q];
+    }
+}
+// dst[afrag(r, k)] = src[r][k] (0 past nr rows), [kR][K] fp64, K a multiple of kCompute / kR
+__device__ __forceinline__ void fill_f64(double *dst, const double *src, int K, int nr) {
+    constexpr int kBatch = 8;
+    for (int i0 = threadIdx.x; i0 < kR * K; i0 += kBatch * kCompute) {
+        double v[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+            const int i = i0 + q * kCompute;
+            v[q] = (i < kR * K && i / K < nr) ? __ldcg(src + i) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+            const int i = i0 + q * kCompute;
+            if (i < kR * K) dst[afrag(i / K, i % K)] = v[q];
+        }
+    }
+}
+
 // The weight chunks of a CTA's whole run form one sequence through the
-// two-slot ring: per batch, the message (or B) GEMM's chunks of kChunkM K-rows
-// (n1 of them, 0 for the GGNN GRU), then the gate phase's chunks of kChunkG
-// K-rows of all six gate matrices (n2).  Thread 0 issues chunk s + 2 as soon
-// as chunk s is consumed -- across phases and batches -- and the first two
-// right after the grid dependency, before the batch's operand loads.
+// kSlots-deep ring: per batch, the message (or B) GEMM's chunks of kChunkM
+// K-rows (n1 of them, 0 for the GGNN GRU), then the gate phase's chunks of
+// kChunkG K-rows of all six gate matrices (n2).  A producer warp issues chunk
+// s + kSlots as soon as every MMA warp has released chunk s -- across phases
+// and batches -- so the MMA warps never wait on one another for the ring.
 struct Feed {
     Ring *ring;
     double *slots;
@@ -94,9 +137,9 @@ struct Feed {
     uint32_t total;              // chunks of the CTA's run
     __device__ void issue(uint32_t seq) const {
         if (seq >= total) return;
-        double *dst = slots + (seq & 1) * (kSlot / 8);
+        double *dst = slots + (seq % kSlots) * (kSlot / 8);
         const int local = (int)(seq % (uint32_t)(n1 + n2));
-        uint64_t *bar = &ring->full[seq & 1];
+        uint64_t *bar = &ring->full[seq % kSlots];
         if (local < n1) {
             ptx::mbar_arrive_expect_tx(bar, kChunkM * kF * 8);
             ptx::bulk_g2s(dst, W1 + (int64_t)local * kChunkM * kF, kChunkM * kF * 8, bar);
@@ -110,13 +153,20 @@ struct Feed {
     }
     // wait for chunk seq; returns its slot
     __device__ const double *wait(uint32_t seq) const {
-        ptx::mbar_wait(&ring->full[seq & 1], (seq >> 1) & 1);
-        return slots + (seq & 1) * (kSlot / 8);
+        ptx::mbar_wait(&ring->full[seq % kSlots], (seq / kSlots) & 1);
+        return slots + (seq % kSlots) * (kSlot / 8);
     }
-    // every thread is done with chunk seq: refill its slot
+    // this warp is done with chunk seq
     __device__ void release(uint32_t seq) const {
-        __syncthreads();
-        if (threadIdx.x == 0) issue(seq + 2);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&ring->empty[seq % kSlots]);
+    }
+    // the producer warp's loop (one thread)
+    __device__ void produce() const {
+        for (uint32_t seq = 0; seq < total; ++seq) {
+            if (seq >= kSlots) ptx::mbar_wait(&ring->empty[seq % kSlots], ((seq / kSlots) - 1) & 1);
+            issue(seq);
+        }
     }
 };
 
@@ -150,7 +200,7 @@ __device__ __forceinline__ void stream_mma(double (&acc)[kNT][2], const double *
 }
 
 // smem: ring 2 x kSlot | a[kR][T kF] (gated) | m[kR][kF] | h[kR][kF], fp64, A-fragment order
-size_t smem_bytes(int T) { return 2 * (size_t)kSlot + sizeof(double) * ((size_t)kR * T * kF + 2 * kR * kF); }
+size_t smem_bytes(int T) { return kSlots * (size_t)kSlot + sizeof(double) * ((size_t)kR * T * kF + 2 * kR * kF); }
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gru_heavy_f64(int32_t nh, const int32_t *__restrict__ rows, int32_t T, const double *__restrict__ Sx,
@@ -161,15 +211,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int K = T * kF;
     double *slots = reinterpret_cast<double *>(smem);
     const double *W_type = W64, *W_ih = W64 + (int64_t)K * kF * gated, *W_hh = W_ih + 3 * kF * kF;
-    double *a = reinterpret_cast<double *>(smem + 2 * kSlot);  // [kR][K]      (gated only)
+    double *a = reinterpret_cast<double *>(smem + kSlots * kSlot);  // [kR][K]      (gated only)
     double *m = a + (gated ? kR * K : 0);                       // [kR][kF]
     double *h = m + kR * kF;                                    // [kR][kF]
     __shared__ Ring ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nt0 = warp * kNT, r = lane >> 2, c2 = (lane & 3) * 2;  // this lane's D row and column pair
     if (threadIdx.x == 0) {
-        ptx::mbar_init(&ring.full[0], 1);
-        ptx::mbar_init(&ring.full[1], 1);
+        for (int i = 0; i < kSlots; ++i) {
+            ptx::mbar_init(&ring.full[i], 1);
+            ptx::mbar_init(&ring.empty[i], kCompute / 32);
+        }
         ptx::fence_mbar_init();
     }
     __syncthreads();
@@ -178,24 +230,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Feed fd{&ring, slots, W_type, W_ih, W_hh, gated ? K / kChunkM : 0, kF / kChunkG,
                   (uint32_t)nb * (uint32_t)((gated ? K / kChunkM : 0) + kF / kChunkG)};
 
-    griddep_wait();  // Sx / mx, the weights and the tensor path's output rows come from the call's earlier kernels
-    if (threadIdx.x == 0) {
-        fd.issue(0);
-        fd.issue(1);
+    if (warp == kCompute / 32) {  // producer warp
+        griddep_wait();  // the fp64 weights come from the call's split-weights kernel
+        if (lane == 0) fd.produce();
+        return;
     }
+    // the layer's own inputs (H, the biases, the graph) before the grid dependency
+    float bias[6][kNT][2];
+#pragma unroll
+    for (int t = 0; t < kNT; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = (nt0 + t) * 8 + c2 + e;
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+                bias[g][t][e] = b_ih[g * kF + j];
+                bias[3 + g][t][e] = b_hh[g * kF + j];
+            }
+        }
+    if ((int)blockIdx.x * kR < nh) fill_rows_f32(h, H, rows, blockIdx.x * kR, min(kR, nh - (int)blockIdx.x * kR));
+    griddep_wait();  // Sx / mx and the tensor path's output rows come from the call's earlier kernels
     for (int32_t b0 = blockIdx.x * kR; b0 < nh; b0 += gridDim.x * kR) {
         const int nr = min(kR, nh - b0);
-        for (int i = threadIdx.x; i < kR * kF; i += kThreads) {
-            const int rr = i / kF, j = i % kF;
-            h[afrag(rr, j)] = rr < nr ? (double)H[(int64_t)rows[b0 + rr] * kF + j] : 0.0;
-            if (!gated) m[afrag(rr, j)] = rr < nr ? mx[(int64_t)(b0 + rr) * kF + j] : 0.0;
-        }
+        if (b0 != (int32_t)blockIdx.x * kR) fill_rows_f32(h, H, rows, b0, nr);
         if (gated)
-            for (int i = threadIdx.x; i < kR * K; i += kThreads) {
-                const int rr = i / K, k = i % K;
-                a[afrag(rr, k)] = rr < nr ? Sx[(int64_t)b0 * K + i] : 0.0;
-            }
-        __syncthreads();
+            fill_f64(a, Sx + (int64_t)b0 * K, K, nr);
+        else
+            fill_f64(m, mx + (int64_t)b0 * kF, kF, nr);
+        compute_sync();
         if (gated) {
             // m = S . W_type  (W_type [T][kF][kF] = [K][kF])
             double acc[kNT][2] = {};
@@ -206,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m[afrag(r, col)] = acc[t][0];
                 m[afrag(r, col + 1)] = acc[t][1];
             }
-            __syncthreads();
+            compute_sync();
         }
         // gate pre-activations: gi[g] = m . W_ih[g], gh[g] = h . W_hh[g] (g = r, z, n); the six
         // matrices stream together in chunks of kChunkG K-rows, [mat][kChunkG / 4][kF / 8][32] per slot
@@ -236,13 +298,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int j = (nt0 + t) * 8 + c2 + e;
-                    const double rg = 1.0 / (1.0 + exp(-(gi[0][t][e] + b_ih[j] + gh[0][t][e] + b_hh[j])));
-                    const double zg = 1.0 / (1.0 + exp(-(gi[1][t][e] + b_ih[kF + j] + gh[1][t][e] + b_hh[kF + j])));
-                    const double n = tanh(gi[2][t][e] + b_ih[2 * kF + j] + rg * (gh[2][t][e] + b_hh[2 * kF + j]));
+                    const double rg = 1.0 / (1.0 + exp(-(gi[0][t][e] + bias[0][t][e] + gh[0][t][e] + bias[3][t][e])));
+                    const double zg = 1.0 / (1.0 + exp(-(gi[1][t][e] + bias[1][t][e] + gh[1][t][e] + bias[4][t][e])));
+                    const double n = tanh(gi[2][t][e] + bias[2][t][e] + rg * (gh[2][t][e] + bias[5][t][e]));
                     o[j] = (float)((1.0 - zg) * n + zg * h[afrag(r, j)]);
                 }
         }
-        __syncthreads();  // m, h, a are rewritten by the next batch
+        compute_sync();  // m, h, a are rewritten by the next batch
     }
 }
 
@@ -253,31 +315,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const double *__restrict__ W_b, const float *__restrict__ b_e, double *__restrict__ Bx) {
     extern __shared__ __align__(16) uint8_t smem[];
     double *slots = reinterpret_cast<double *>(smem);
-    double *hs = reinterpret_cast<double *>(smem + 2 * kSlot);  // [kR][kF], A-fragment order
+    double *hs = reinterpret_cast<double *>(smem + kSlots * kSlot);  // [kR][kF], A-fragment order
     __shared__ Ring ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nt0 = warp * kNT, r = lane >> 2, c2 = (lane & 3) * 2;
     if (threadIdx.x == 0) {
-        ptx::mbar_init(&ring.full[0], 1);
-        ptx::mbar_init(&ring.full[1], 1);
+        for (int i = 0; i < kSlots; ++i) {
+            ptx::mbar_init(&ring.full[i], 1);
+            ptx::mbar_init(&ring.empty[i], kCompute / 32);
+        }
         ptx::fence_mbar_init();
     }
     __syncthreads();
     uint32_t cc = 0;
     const int nb = (nh - (int)blockIdx.x * kR + (int)gridDim.x * kR - 1) / ((int)gridDim.x * kR);
     const Feed fd{&ring, slots, W_b, nullptr, nullptr, kF / kChunkM, 0, (uint32_t)nb * (uint32_t)(kF / kChunkM)};
-    griddep_wait();  // the weights come from the call's split-weights kernel
-    if (threadIdx.x == 0) {
-        fd.issue(0);
-        fd.issue(1);
+    if (warp == kCompute / 32) {  // producer warp
+        griddep_wait();  // the fp64 weights come from the call's split-weights kernel
+        if (lane == 0) fd.produce();
+        return;
     }
     for (int32_t b0 = blockIdx.x * kR; b0 < nh; b0 += gridDim.x * kR) {
         const int nr = min(kR, nh - b0);
-        for (int i = threadIdx.x; i < kR * kF; i += kThreads) {
-            const int rr = i / kF, j = i % kF;
-            hs[afrag(rr, j)] = rr < nr ? (double)H[(int64_t)rows[b0 + rr] * kF + j] : 0.0;
-        }
-        __syncthreads();
+        fill_rows_f32(hs, H, rows, b0, nr);  // the layer input: before the grid dependency
+        if (b0 == (int32_t)blockIdx.x * kR) griddep_wait();  // before this grid's first global write
+        compute_sync();
         double acc[kNT][2] = {};
         stream_mma(acc, hs, kF, fd, cc, nt0, lane);
         if (r < nr)
@@ -288,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int j = (nt0 + t) * 8 + c2 + e;
                     Bx[(int64_t)(b0 + r) * kF + j] = acc[t][e] + (b_e ? (double)b_e[j] : 0.0);
                 }
-        __syncthreads();
+        compute_sync();
     }
 }
 
