@@ -38,14 +38,17 @@
 // (8 rows x 4 k, one double per lane) feeds two MMAs and each weight double
 // read from shared memory feeds 8 FMAs inside the MMA.  The operands sit in
 // shared memory in fragment order -- A as [k/4][row][k%4], the weights as
-// [k/4][n/8][n%8][k%4] (permuted once per call by k_weights_f64) -- so every
-// fragment load is one conflict-free 256-byte LDS.64.  The weights stream
-// through a two-slot ring of 48 KB chunks filled by bulk copies (one thread)
-// while the previous chunk is consumed.
-// Measured on the way (C4): the FFMA form with thread = (4 rows, column) was
-// bound by shared-memory wavefronts (one LDS per DFMA: 48 us); before it,
-// weights read from L2 per FMA (60 us), fp32 weights converted per use (F2F on
-// the XU pipe, 66 us) and a (row, column-quad) mapping (107 us).
+// [k/4][n/8][n%8][k%4] (permuted once per call by the split-weights kernel,
+// heavy_weights_f64_item) -- so every fragment load is one conflict-free
+// 256-byte LDS.64.  The weights stream through a 3-slot ring of 48 KB chunks
+// filled by bulk copies from a producer warp.
+// Measured (C4 / C8 heavy GRU, in-step): 26.8 / 18.5 us, DMMA pipe ~42% busy
+// on the 105 SMs that hold a batch.  On the way: the FFMA form with thread =
+// (4 rows, column) was bound by shared-memory wavefronts (one LDS per DFMA:
+// 48.9 / 24 us); before it, weights read from L2 per FMA (60 us), fp32
+// weights converted per use (F2F on the XU pipe, 66 us) and a (row,
+// column-quad) mapping (107 us); serial operand fills (one round trip per
+// element loop) were 30% of the DMMA form's stall samples.
 #include <cuda_runtime.h>
 
 #include <cstdint>
