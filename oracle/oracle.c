@@ -239,8 +239,8 @@ static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
  * Gather sums the in-edge messages, ApplyVertex is a GRU) and Table 1 line
  * 178; BASELINE.json config C4 fixes a per-edge-type message weight W_t and
  * the GRU shapes (readings A6, A15, A16):
- *   S_t[v] = sum_{e=(u->v), type(e)=t} H[u]           (Gather, per type)
- *   m[v]   = sum_t S_t[v] . W_t                        (W_t: [f][f])
+ *   msg_e  = H[u] . W_{type(e)}   for e = (u -> v)     (ApplyEdge, per edge; W_t: [f][f])
+ *   m[v]   = sum_{e=(u->v)} msg_e                      (Gather, sum)
  *   r  = sigma(m W_ir + b_ir + h W_hr + b_hr)
  *   zg = sigma(m W_iz + b_iz + h W_hz + b_hz)
  *   ng = tanh (m W_in + b_in + r * (h W_hn + b_hn))
@@ -257,7 +257,7 @@ void oracle_gated(int32_t n, const int64_t *row_ptr, const int32_t *col_src, con
     if (!rows) nrows = n;
 #pragma omp parallel
     {
-        double *S = (double *)malloc(sizeof(double) * (size_t)num_etypes * (size_t)f);
+        double *xu = (double *)malloc(sizeof(double) * (size_t)f);
         double *m = (double *)malloc(sizeof(double) * (size_t)f);
         double *h = (double *)malloc(sizeof(double) * (size_t)f);
         double *gi = (double *)malloc(sizeof(double) * 3 * (size_t)hid);
@@ -265,16 +265,16 @@ void oracle_gated(int32_t n, const int64_t *row_ptr, const int32_t *col_src, con
 #pragma omp for schedule(dynamic, 64)
         for (int64_t i = 0; i < nrows; ++i) {
             int64_t v = row_at(rows, i);
-            for (int64_t q = 0; q < (int64_t)num_etypes * f; ++q) S[q] = 0.0;
-            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {
-                int32_t t = etype_csr ? etype_csr[p] : 0;
-                for (int32_t k = 0; k < f; ++k) S[(int64_t)t * f + k] += load_x(x, x_dtype, col_src[p], f, k);
-            }
             for (int32_t j = 0; j < f; ++j) m[j] = 0.0;
-            for (int32_t t = 0; t < num_etypes; ++t)
-                for (int32_t k = 0; k < f; ++k)
-                    for (int32_t j = 0; j < f; ++j)
-                        m[j] += S[(int64_t)t * f + k] * W_type[((int64_t)t * f + k) * f + j];
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {   /* in-edges in CSR order */
+                int32_t t = etype_csr ? etype_csr[p] : 0;
+                for (int32_t k = 0; k < f; ++k) xu[k] = load_x(x, x_dtype, col_src[p], f, k);   /* Scatter */
+                for (int32_t j = 0; j < f; ++j) {                                              /* ApplyEdge */
+                    double msg = 0.0;
+                    for (int32_t k = 0; k < f; ++k) msg += xu[k] * W_type[((int64_t)t * f + k) * f + j];
+                    m[j] += msg;                                                               /* Gather */
+                }
+            }
             for (int32_t k = 0; k < f; ++k) h[k] = load_x(x, x_dtype, v, f, k);
             for (int32_t g = 0; g < 3; ++g)
                 for (int32_t j = 0; j < hid; ++j) {
@@ -295,7 +295,7 @@ void oracle_gated(int32_t n, const int64_t *row_ptr, const int32_t *col_src, con
                 o[j] = (1.0 - zg) * ng + zg * h[j];
             }
         }
-        free(S); free(m); free(h); free(gi); free(gh);
+        free(xu); free(m); free(h); free(gi); free(gh);
     }
 }
 
@@ -320,25 +320,22 @@ void oracle_rgcn(int32_t n, const int64_t *row_ptr, const int32_t *col_src, cons
     if (!rows) nrows = n;
 #pragma omp parallel
     {
-        double *S = (double *)malloc(sizeof(double) * (size_t)num_etypes * (size_t)f);
+        double *xu = (double *)malloc(sizeof(double) * (size_t)f);
         int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (size_t)num_etypes);
 #pragma omp for schedule(dynamic, 64)
         for (int64_t i = 0; i < nrows; ++i) {
             int64_t v = row_at(rows, i);
-            for (int64_t q = 0; q < (int64_t)num_etypes * f; ++q) S[q] = 0.0;
             for (int32_t t = 0; t < num_etypes; ++t) cnt[t] = 0;
-            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {        /* Gather: per-type sums */
-                int32_t t = etype_csr ? etype_csr[p] : 0;
-                cnt[t] += 1;
-                for (int32_t k = 0; k < f; ++k) S[(int64_t)t * f + k] += load_x(x, x_dtype, col_src[p], f, k);
-            }
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) cnt[etype_csr ? etype_csr[p] : 0] += 1;  /* c_{v,t} */
             double *o = out + i * (int64_t)f_out;
             for (int32_t j = 0; j < f_out; ++j) o[j] = b ? b[j] : 0.0;
-            for (int32_t t = 0; t < num_etypes; ++t) {                        /* ApplyEdge by type, mean */
-                if (cnt[t] == 0) continue;
-                for (int32_t k = 0; k < f; ++k) {
-                    double s = S[(int64_t)t * f + k] / (double)cnt[t];
-                    for (int32_t j = 0; j < f_out; ++j) o[j] += s * W_type[((int64_t)t * f + k) * f_out + j];
+            for (int64_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p) {   /* per in-edge, CSR order */
+                int32_t t = etype_csr ? etype_csr[p] : 0;
+                for (int32_t k = 0; k < f; ++k) xu[k] = load_x(x, x_dtype, col_src[p], f, k);   /* Scatter */
+                for (int32_t j = 0; j < f_out; ++j) {                                          /* ApplyEdge */
+                    double msg = 0.0;
+                    for (int32_t k = 0; k < f; ++k) msg += xu[k] * W_type[((int64_t)t * f + k) * f_out + j];
+                    o[j] += msg / (double)cnt[t];                                              /* Gather, mean */
                 }
             }
             for (int32_t k = 0; k < f; ++k) {                                 /* the vertex's own term */
@@ -348,7 +345,7 @@ void oracle_rgcn(int32_t n, const int64_t *row_ptr, const int32_t *col_src, cons
             if (act == 1)
                 for (int32_t j = 0; j < f_out; ++j) o[j] = o[j] > 0.0 ? o[j] : 0.0;
         }
-        free(S);
+        free(xu);
         free(cnt);
     }
 }

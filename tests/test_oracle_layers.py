@@ -244,6 +244,40 @@ def test_gated_dense_and_grucell(name, n, s, d):
     np.testing.assert_allclose(y, gru_torch(m, H, Wih, Whh, bih, bhh), rtol=1e-11, atol=1e-12)
 
 
+def test_gated_messages_per_edge():
+    """ApplyEdge is per edge: m[v] = sum over in-edges
+    e = (u -> v) of H[u] . W_type(e), summed edge by edge with np.add.at and
+    no per-type grouping, against the oracle's GRU of it (a wrong type index
+    or a transposed W_t fails here)."""
+    n, T, f = 30, 3, 5
+    s, d = zoo.random_multigraph(n, 150, 21)
+    et = (np.arange(150) * 5 % T).astype(np.int32)
+    H = RNG.standard_normal((n, f))
+    Wt, Wih, Whh, bih, bhh = gated_params(f, T)
+    msgs = np.einsum("ek,ekj->ej", H[s], Wt[et])
+    m = np.zeros((n, f))
+    np.add.at(m, d, msgs)
+    y = oracle.gated(oracle.csr_build(n, s, d, et, T), H, Wt, Wih, Whh, bih, bhh)
+    np.testing.assert_allclose(y, gru_torch(m, H, Wih, Whh, bih, bhh), rtol=1e-11, atol=1e-12)
+
+
+def test_rgcn_messages_per_edge():
+    """R-GCN (reading A24): out[v] = act(sum_e H[u] W_type(e) / c_{v,type(e)} +
+    H[v] W_self + b), accumulated edge by edge."""
+    n, T, f, fo = 25, 4, 4, 3
+    s, d = zoo.random_multigraph(n, 120, 22)
+    et = (np.arange(120) * 3 % T).astype(np.int32)
+    X = RNG.standard_normal((n, f))
+    Wt, Ws, b = RNG.standard_normal((T, f, fo)), RNG.standard_normal((f, fo)), RNG.standard_normal(fo)
+    c = np.zeros((n, T))
+    np.add.at(c, (d, et), 1.0)
+    msgs = np.einsum("ek,ekj->ej", X[s], Wt[et]) / c[d, et][:, None]
+    ref = X @ Ws + b
+    np.add.at(ref, d, msgs)
+    y = oracle.rgcn(oracle.csr_build(n, s, d, et, T), X, Wt, Ws, b, act=0)
+    np.testing.assert_allclose(y, ref, rtol=1e-11, atol=1e-12)
+
+
 def test_gated_gru_closed_forms():
     s, d = zoo.random_multigraph(40, 200, 9)
     et = (np.arange(200) % 4).astype(np.int32)
