@@ -401,6 +401,13 @@ __global__ void k_compact_rows(int32_t n, const int32_t *__restrict__ aflag, con
     }
 }
 // warp per compact row: its in-edges, in CSR order
+// the complement of the aggregation rows: erow[v - apos[v]] = v where aflag[v] == 0
+__global__ void k_compact_epi_rows(int32_t n, const int32_t *__restrict__ aflag, const int64_t *__restrict__ apos,
+                                   int32_t *erow) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (!aflag[v]) erow[v - apos[v]] = (int32_t)v;
+}
+
 __global__ void k_compact_edges(int32_t an, const int32_t *__restrict__ arow, const int64_t *__restrict__ row_ptr,
                                 const int32_t *__restrict__ col_src, const int64_t *__restrict__ arow_ptr,
                                 int32_t *acol_src) {
@@ -505,7 +512,8 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     SAGA_TRY(merge_path_schedule(n, e, g->row_ptr, &g->ftask_items, &g->fntasks, &g->ftask_v, &g->ftask_p, st, 128));
 
     // 8. aggregation view (see GraphDev): rows with only a self-loop or no
-    //    in-edge are finished by the GCN GEMM epilogue; a compacted CSR of the
+    //    in-edge are finished outside the gather (GAT: the GEMM epilogue;
+    //    GCN: a streaming pass over their list erow); a compacted CSR of the
     //    others (a second host sync, for its sizes)
     if (n > 0) {
         int32_t *aflag, *adeg = nullptr;
@@ -546,6 +554,12 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
             SAGA_TRY(cudaGetLastError());
             SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->aftask_items, &g->afntasks, &g->aftask_v,
                                          &g->aftask_p, st, 128));
+            SAGA_TRY(merge_path_schedule(g->an, g->ae, g->arow_ptr, &g->atask_items, &g->antasks, &g->atask_v,
+                                         &g->atask_p, st, 32));
+            g->ne = (int32_t)(n - an);
+            SAGA_TRY(cudaMallocAsync(&g->erow, sizeof(int32_t) * (size_t)std::max<int32_t>(g->ne, 1), st));
+            k_compact_epi_rows<<<grid_for(n, 256), 256, 0, st>>>(n, aflag, apos, g->erow);
+            SAGA_TRY(cudaGetLastError());
             cudaFreeAsync(adeg, st);
         }
         cudaFreeAsync(aflag, st);
@@ -594,7 +608,7 @@ void free_graph(GraphDev *g) {
     void *ptrs[] = {g->row_ptr,  g->col_src,  g->edge_id,  g->etype,   g->in_deg,  g->out_deg, g->dinv,
                     g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->arow, g->arow_ptr,
                     g->acol_src, g->adinv, g->aftask_v, g->aftask_p, g->trow_ptr, g->tcol_src, g->tinv_deg,
-                    g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p};
+                    g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p, g->atask_v, g->atask_p, g->erow};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, st);
 }

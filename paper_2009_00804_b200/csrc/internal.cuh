@@ -97,7 +97,8 @@ struct GraphDev {
     int64_t *ttask_p = nullptr;
     // Aggregation view (built when some rows' in-edges are nothing but one
     // self-loop, or none): those rows' GAT output (ELU(z[v]), or 0) is written
-    // by the GEMM epilogue, and the edge softmax runs over a compacted CSR of
+    // by the GEMM epilogue, their GCN output act(dinv[v] Y[v] + b) by a
+    // streaming pass over erow, and the gathers run over a compacted CSR of
     // the other rows only (row i = vertex arow[i]).
     int32_t an = 0;               // host: aggregation rows
     int64_t ae = 0;               // host: their in-edges
@@ -108,6 +109,11 @@ struct GraphDev {
     int64_t aftask_items = 0, afntasks = 0;  // its merge-path schedule (the 4x finer one, GAT)
     int32_t *aftask_v = nullptr;
     int64_t *aftask_p = nullptr;
+    int64_t atask_items = 0, antasks = 0;    // its one-task-per-warp schedule (GCN)
+    int32_t *atask_v = nullptr;
+    int64_t *atask_p = nullptr;
+    int32_t ne = 0;               // host: the other rows (self-loop only, or no in-edge): n - an
+    int32_t *erow = nullptr;      // [ne]  their vertices, ascending
     cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
 };
 

@@ -175,7 +175,7 @@ struct Plan {
 Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o) {
     Plan p;
     // the typed gathers run over the typed view's own schedule
-    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks, g.afntasks});
+    const size_t nt = (size_t)std::max({g.ntasks, g.tntasks, g.fntasks, g.afntasks, g.antasks});
     const size_t n = (size_t)g.n;
     size_t width = 0;
     switch (kind) {
@@ -478,7 +478,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
     // split-row tickets start at 0; every ticket's winner resets its counter,
     // so a completed call leaves them zero (opts.workspace_zeroed skips this)
     if (!o.workspace_zeroed && !(kind == SAGA_GCN && x->dtype == SAGA_F32 && gcn_f32_rowwise(d))) {
-        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks, d.afntasks}),
+        e = cudaMemsetAsync(aw.counters, 0, sizeof(int32_t) * (size_t)std::max({d.ntasks, d.tntasks, d.fntasks, d.afntasks, d.antasks}),
                             st);
         if (e) return cuda_fail(e, "memset counters");
     }
