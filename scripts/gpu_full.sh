@@ -9,6 +9,7 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/$TAG
 timeout 900 python bench.py > gpurun_out/$TAG/bench_C5.json 2> gpurun_out/$TAG/bench_C5.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/$TAG/bench_ref_C5.json 2> gpurun_out/$TAG/bench_ref_C5.err
 for c in C1 C2 C3 C4 C6 C7 C8; do timeout 600 python bench.py --config $c > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err; done
+for c in C1 C2 C3 C4 C5 C6 C7 C8; do timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --e2e-steps 0 --timeline gpurun_out/$TAG/timeline_$c.json > /dev/null 2>&1; done
 for c in C1 C2 C3 C4 C5 C6 C7 C8; do python -c "import json;j=json.load(open('gpurun_out/$TAG/bench_$c.json'));print('$c', round(j['ms_per_step'],4), j['value'], {k:round(v['avg_ms'],4) for k,v in j['config']['per_kernel'].items()})"; done
 # ncu: launch list of the default bench command (plain run first)
 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/plain.log 2>&1 && \
@@ -16,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_launch.log 2>&1
 for c in C5 C3 C4 C2 C1 C6 C7 C8; do
   timeout 300 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/plain_$c.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_weights_f64|k_split' -s 3 -c 9 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_gcn_epi|k_split' -s 3 -c 9 \
       -o gpurun_out/$TAG/full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_full_$c.log 2>&1
 done
 ls gpurun_out/$TAG

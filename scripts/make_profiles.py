@@ -22,14 +22,14 @@ LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)
     "C2": [("SumBf16Op", "agg_mean_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C3": [("GatOp", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
     "C4": [("SumF32Op", "agg_typed_f32"), ("k_gemm_tf32split", "gated_apply_tf32x3"), ("k_split_weights", "gated_apply_tf32x3"),
-           ("k_gru_heavy_f64", "gru_heavy_f64"), ("k_weights_f64", "gru_heavy_f64")],
-    "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
+           ("k_gru_heavy_f64", "gru_heavy_f64")],
+    "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gcn_epi_rows", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C6": [("SumF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3"), ("k_split_rgcn", "rgcn_apply_tf32x3")],
     "C7": [("k_lstm_gather", "lstm_gather"), ("k_stage_whh", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C8": [("EdgeMlpOp", "agg_edge_mlp_f32"), ("k_gemm_tf32split<256", "ggnn_gru_tf32x3"),
            ("k_gemm_i8x", "ggnn_edge_i8x"), ("k_slice_rows", "ggnn_edge_i8x"), ("k_slice_wt_ggnn", "ggnn_edge_i8x"),
            ("k_split_ggnn", "ggnn_split_weights"), ("k_ggnn_heavy_b", "ggnn_heavy_b_f64"),
-           ("k_weights_f64", "ggnn_heavy_b_f64"), ("k_gru_heavy_f64", "gru_heavy_f64")],
+           ("k_gru_heavy_f64", "gru_heavy_f64")],
 }
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram_read"),
         ("dram__bytes_write.sum", "dram_write"), ("lts__t_sector_hit_rate.pct", "L2_hit_%"),
