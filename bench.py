@@ -200,25 +200,11 @@ def algorithmic(cfg, gs=None):
         out["sage_fused_tc"] = {"bytes": (e * 4 + (n + 1) * 8 + n * 4 + n * (f0 + f1) * 2 + n * (f1 + f2) * 2) // 2,
                                 "flops": (e * (f0 + f1) + 2 * n * (2 * f0 * f1 + 2 * f1 * f2)) // 2, "peak": "hbm"}
     elif cfg.model == "sage":
-        f0, f1, f2 = cfg.dims   # two layers f0 -> f1 -> f2
-        base = e * 4 + (n + 1) * 8 + n * 4  # col_src, row_ptr, 1/deg
-        # a layer with out < in projects first (saga_host.cu): ZS = X [W_neigh | W_self], then the
-        # mean of the out-wide Z rows plus S (agg_sage_proj_bf16); else mean of X (M written), then
-        # the concat GEMM; per label the mean over its launches
-        agg, proj, gemm = [], [], []
-        for fi, fo in ((f0, f1), (f1, f2)):
-            if fo < fi:
-                proj.append((base + n * fo * 2 * 3, e * fo))            # Z read, S read, out written
-                gemm.append((n * 2 * (fi + 2 * fo), 2 * n * fi * 2 * fo))
-            else:
-                agg.append((base + n * fi * 2 * 2, e * fi))              # X read, M written
-                gemm.append((n * 2 * (2 * fi + fo), 2 * n * 2 * fi * fo))
-        for lab, lst in (("agg_mean_bf16", agg), ("agg_sage_proj_bf16", proj)):
-            if lst:
-                out[lab] = {"bytes": sum(b for b, _ in lst) // len(lst), "flops": sum(f for _, f in lst) // len(lst),
-                            "peak": "hbm"}
-        out["gemm_bf16_tc"] = {"bytes": sum(b for b, _ in gemm) // 2, "flops": sum(f for _, f in gemm) // 2,
-                               "peak": "tensor_bf16"}
+        f0, f1, f2 = cfg.dims   # two layers: agg widths f0, f1; GEMMs 2f0 -> f1, 2f1 -> f2 (mean of the two launches)
+        out["agg_mean_bf16"] = {"bytes": e * 4 + (n + 1) * 8 + n * 4 + n * (f0 + f1) * 2 * 2 // 2,
+                                "flops": e * (f0 + f1) // 2, "peak": "hbm"}
+        out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f0 + f1 + 2 * f1 + f2) // 2,
+                               "flops": 2 * n * (2 * f0 * f1 + 2 * f1 * f2) // 2, "peak": "tensor_bf16"}
     elif cfg.model == "gat":
         fi, fo = cfg.dims
         if gs is None:
@@ -658,7 +644,6 @@ STAGES = {
     "gcn_f32_fused": "S3+S4+S5 Scatter/Gather/ApplyVertex (fused)",
     "agg_gcn_bf16": "S3+S4 Scatter/Gather (+S5 epilogue)",
     "agg_mean_bf16": "S3+S4 Scatter/Gather",
-    "agg_sage_proj_bf16": "S3+S4 Scatter/Gather (+S5 epilogue)",
     "agg_typed_f32": "S3+S4 Scatter/Gather",
     "agg_typed_mean_f32": "S3+S4 Scatter/Gather",
     "gat_edge": "S3+S4 Scatter/ApplyEdge/Gather (+S5 epilogue)",

@@ -276,82 +276,6 @@ struct GcnF32FusedOp {
     }
 };
 
-// GraphSAGE-mean with the projection ahead of the Gather (out_dim < in_dim,
-// C2's second layer): one GEMM makes ZS = X [W_neigh | W_self] (bf16
-// [n][2 f], f = 32 NB), and out[v] = act(mean_{u->v} Z[u] + S[v] + b) -- by
-// linearity the same layer (concat then GEMM), while the Gather
-// moves f instead of in_dim values per edge.  S[v] is read when the row
-// starts (begin_row), so the flush has no dependent load.
-template <int kAct, int NB>
-struct SageProjOp {
-    static constexpr int kWin = 1;
-    static constexpr int kSlot = 32 * NB;
-    static constexpr bool kSplitBatch = true;  // narrow rows, as SumBf16Op's
-    __device__ static int win_col(int) { return 0; }
-    struct Acc { float a[NB]; uint32_t s[NB / 2]; };
-    using Val = typename SumBf16Op<kAct, NB>::Val;
-    const __nv_bfloat16 *ZS;  // [n][2 f]: Z then S
-    const float *scale;       // 1 / in-degree (0 without in-edges)
-    const float *bias;
-    __nv_bfloat16 *out;       // [n][f]
-    __device__ __forceinline__ float row_value(int32_t v, int) const { return __ldg(scale + v); }
-    __device__ __forceinline__ void zero(Acc &c) const {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) c.a[i] = 0.0f;
-    }
-    __device__ __forceinline__ const char *row(int32_t u, int lane) const {
-        return ptx::mad_wide((uint32_t)u, 128u * NB, reinterpret_cast<const char *>(ZS) + lane * (2 * NB));
-    }
-    __device__ __forceinline__ void begin_row(Acc &c, int32_t v, int lane) const {
-        const char *p = row(v, lane) + 64 * NB;
-        if constexpr (NB == 4) {
-            const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
-            c.s[0] = x.x; c.s[1] = x.y;
-        } else {
-            c.s[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
-        }
-    }
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        const char *p = row(u, lane);
-        Val v;
-        if constexpr (NB == 4) {
-            const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
-            v.w[0] = x.x; v.w[1] = x.y;
-        } else {
-            v.w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
-        }
-        return v;
-    }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, float) const {
-#pragma unroll
-        for (int i = 0; i < NB / 2; ++i) ptx::add_bf16x2_f32(c.a[2 * i], c.a[2 * i + 1], v.w[i]);
-    }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float rs, int lane, const float *Ws) const {
-        uint32_t pk[NB / 2];
-#pragma unroll
-        for (int h = 0; h < NB / 2; ++h) {
-            const float2 sv = ptx::unpack_bf16x2(c.s[h]);
-            float2 b = make_float2(0.f, 0.f);
-            if (bias) b = reinterpret_cast<const float2 *>(Ws + lane * NB)[h];
-            pk[h] = ptx::pack_bf16x2(act_fn(fmaf(rs, c.a[2 * h], sv.x + b.x), kAct),
-                                     act_fn(fmaf(rs, c.a[2 * h + 1], sv.y + b.y), kAct));
-        }
-        char *p = reinterpret_cast<char *>(out + (int64_t)v * (32 * NB)) + lane * (2 * NB);
-        if constexpr (NB == 4)
-            *reinterpret_cast<uint2 *>(p) = make_uint2(pk[0], pk[1]);
-        else
-            *reinterpret_cast<uint32_t *>(p) = pk[0];
-    }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) slot[lane * NB + i] = c.a[i];
-    }
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) c.a[i] += __ldcg(slot + lane * NB + i);
-    }
-};
-
 // C3: GAT.  Lane L owns head h = L / 4 and output columns 2L, 2L+1 (a 4-byte
 // slice of the 128-byte z row).  Per edge s = LeakyReLU(el[u,h] + er[v,h])
 // (the additive form of a^T [z_u || z_v], reading A14) and a single-exp
@@ -1216,22 +1140,6 @@ cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
                                  AggWorkspace ws, cudaStream_t st) {
     return agg_sum_bf16<SAGA_ACT_NONE>(view(g), X, f, g.inv_deg, nullptr, M, ws, st);
-}
-
-cudaError_t launch_agg_sage_proj_bf16(const GraphDev &g, const __nv_bfloat16 *ZS, int32_t f, const float *bias, int act,
-                                      __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    const int32_t wb = bias ? f : 0;
-    if (f == 64) {
-        if (act == SAGA_ACT_RELU)
-            return run<8, 4>(view(g), SageProjOp<SAGA_ACT_RELU, 2>{ZS, g.inv_deg, bias, out}, ws, st, bias, wb);
-        return run<8, 4>(view(g), SageProjOp<SAGA_ACT_NONE, 2>{ZS, g.inv_deg, bias, out}, ws, st, bias, wb);
-    }
-    if (f == 128) {
-        if (act == SAGA_ACT_RELU)
-            return run<8, 4>(view(g), SageProjOp<SAGA_ACT_RELU, 4>{ZS, g.inv_deg, bias, out}, ws, st, bias, wb);
-        return run<8, 4>(view(g), SageProjOp<SAGA_ACT_NONE, 4>{ZS, g.inv_deg, bias, out}, ws, st, bias, wb);
-    }
-    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in, const float *W, int32_t f_out,

@@ -66,10 +66,6 @@ struct EpiParams {
     const float *a_src, *a_dst;
     float *el, *er;
     bool self_out;  // GAT: the aggregation view's output tile (GemmArgs::out2; kernel template SELF)
-    // W's columns [0, n1) are rows of W (row stride ld0), columns [n1, N) rows
-    // of w2 (row stride ld1) -- GemmArgs::W2; by default n1 = N, ld0 = N
-    const __nv_bfloat16 *w2;
-    int n1, ld0, ld1;
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -190,19 +186,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // One unit = an 8(k) x 8(n) block: eight independent 16-byte loads
             // along n (coalesced across threads), a register transpose, eight
             // 16-byte smem stores (one K-major chunk per n).
-            // element (k, n) of W: rows of W for n < n1, of w2 beyond
-            auto wsrc = [&](int k, int n) -> const __nv_bfloat16 * {
-                return n < ep.n1 ? W + (int64_t)k * ep.ld0 + n : ep.w2 + (int64_t)k * ep.ld1 + (n - ep.n1);
-            };
-            const bool w_vec = ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(ep.w2)) & 15) == 0 &&
-                               ((ep.ld0 | ep.ld1 | ep.n1) & 7) == 0;
-            if (w_vec) {
+            if ((reinterpret_cast<uintptr_t>(W) & 15) == 0) {
                 const int units = KB * 8 * (BN / 8);
                 auto unit_load = [&](int c, uint4 (&v)[8]) {
                     const int n0 = (c % (BN / 8)) * 8;
                     const int k0 = (c / BN) * kBK + ((c / (BN / 8)) % 8) * 8;
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) v[r] = __ldg(reinterpret_cast<const uint4 *>(wsrc(k0 + r, n0)));
+                    for (int r = 0; r < 8; ++r)
+                        v[r] = __ldg(reinterpret_cast<const uint4 *>(W + (int64_t)(k0 + r) * BN + n0));
                 };
                 auto unit_store = [&](int c, const uint4 (&v)[8]) {
                     const int n0 = (c % (BN / 8)) * 8;
@@ -242,8 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t w[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        __nv_bfloat16 lo = *wsrc(k0 + 2 * i, n);
-                        __nv_bfloat16 hi = *wsrc(k0 + 2 * i + 1, n);
+                        __nv_bfloat16 lo = W[(int64_t)(k0 + 2 * i) * BN + n];
+                        __nv_bfloat16 hi = W[(int64_t)(k0 + 2 * i + 1) * BN + n];
                         w[i] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
                     }
                     uint8_t *dst = Bs + kb * L::kBBytesPerKB + n * 128 + ((kc ^ (n & 7)) << 4);
@@ -460,7 +451,7 @@ cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char *
         return cudaErrorInvalidValue;
     }
     EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er,
-                 a.epi == EPI_GAT && a.out2, a.W2, a.W2 ? a.N1 : a.N, a.W2 ? a.ldw : a.N, a.W2 ? a.ldw2 : 0};
+                 a.epi == EPI_GAT && a.out2};
     const int KB = K / kBK, KB0 = a.K0 / kBK;
     // instantiated modes: GCN (row scale), SAGE / LSTM (bias + act), GAT (N = 64,
     // with / without the aggregation view's output tile)

@@ -143,10 +143,6 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 // SAGE: M[v] = inv_deg[v] * sum x[u]  (bf16 out)
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
                                  AggWorkspace ws, cudaStream_t st);
-// GraphSAGE-mean after the projection (out_dim < in_dim): ZS = X [W_neigh | W_self]
-// bf16 [n][2 f]; out[v] = act(mean Z[u] + S[v] + bias), bf16 [n][f], f in {64, 128}.
-cudaError_t launch_agg_sage_proj_bf16(const GraphDev &g, const __nv_bfloat16 *ZS, int32_t f, const float *bias, int act,
-                                      __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
 // GAT fused edge kernel: online softmax + aggregate + ELU.
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
                             float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
@@ -166,12 +162,6 @@ struct GemmArgs {
     int32_t N = 0;
     const __nv_bfloat16 *A0 = nullptr, *A1 = nullptr;  // [M][K0], [M][K1]
     const __nv_bfloat16 *W = nullptr;                  // [K0+K1][N] row-major
-    // optional second weight source: columns [0, N1) of the GEMM's W are
-    // W[k][n] (row stride ldw), columns [N1, N) are W2[k][n - N1] (row stride
-    // ldw2) -- SAGE's pre-projection [W_neigh | W_self] straight from the
-    // caller's [W_self; W_neigh]
-    const __nv_bfloat16 *W2 = nullptr;
-    int32_t N1 = 0, ldw = 0, ldw2 = 0;
     __nv_bfloat16 *out = nullptr;                      // [M][N]
     GemmEpi epi = EPI_ROWSCALE;
     const float *row_scale = nullptr;                  // EPI_ROWSCALE

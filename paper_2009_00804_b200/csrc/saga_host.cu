@@ -529,36 +529,6 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                 if (e) return fail(SAGA_ECUDA, "sage fused: %s (%s)", cudaGetErrorString(e), why);
                 return SAGA_OK;
             }
-            if (o.out_dim < o.in_dim) {
-                // projection ahead of the Gather (by linearity): ZS = X [W_neigh | W_self]
-                // straight from the caller's W = [W_self; W_neigh], then out = act(mean Z + S + b)
-                // -- the Gather moves out_dim instead of in_dim values per edge
-                __nv_bfloat16 *ZS = reinterpret_cast<__nv_bfloat16 *>(i0);
-                const __nv_bfloat16 *W = static_cast<const __nv_bfloat16 *>(w->W);
-                GemmArgs a;
-                a.M = d.n; a.K0 = o.in_dim; a.K1 = 0; a.N = 2 * o.out_dim;
-                a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
-                a.W = W + (size_t)o.in_dim * o.out_dim;  // W_neigh -> columns [0, out_dim)
-                a.ldw = o.out_dim;
-                a.N1 = o.out_dim;
-                a.W2 = W;                                // W_self -> columns [out_dim, 2 out_dim)
-                a.ldw2 = o.out_dim;
-                a.out = ZS;
-                a.epi = EPI_BIAS_ACT;
-                a.act = SAGA_ACT_NONE;
-                {
-                    ProfScope ps_("gemm_bf16_tc", st);
-                    e = launch_gemm_bf16_tc(a, st, &why);
-                }
-                if (e) return fail(SAGA_ECUDA, "sage projection gemm: %s (%s)", cudaGetErrorString(e), why);
-                {
-                    ProfScope ps_("agg_sage_proj_bf16", st);
-                    e = launch_agg_sage_proj_bf16(d, ZS, o.out_dim, w->bias, o.act,
-                                                  static_cast<__nv_bfloat16 *>(out->data), aw, st);
-                }
-                if (e) return cuda_fail(e, "sage aggregate (projected)");
-                return SAGA_OK;
-            }
             __nv_bfloat16 *M = reinterpret_cast<__nv_bfloat16 *>(i0);
             {
                 ProfScope ps_("agg_mean_bf16", st);

@@ -46,7 +46,7 @@ def test_gat_view_bytes(bench):
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"])
 def test_every_profiled_kernel_has_a_model(bench, cfg):
-    expected = {"C1": {"gcn_f32_fused"}, "C2": {"agg_mean_bf16", "agg_sage_proj_bf16", "gemm_bf16_tc"},
+    expected = {"C1": {"gcn_f32_fused"}, "C2": {"agg_mean_bf16", "gemm_bf16_tc"},
                 "C3": {"gemm_bf16_tc_gat", "gat_edge"}, "C4": {"agg_typed_f32", "gated_apply_tf32x3"},
                 "C5": {"gemm_bf16_tc", "agg_gcn_bf16"}, "C6": {"agg_typed_mean_f32", "rgcn_apply_tf32x3"},
                 "C7": {"lstm_gather", "lstm_input_gemm", "gemm_bf16_tc"},
@@ -58,16 +58,12 @@ def test_every_profiled_kernel_has_a_model(bench, cfg):
 
 
 def test_sage_model_is_per_launch(bench):
-    """C2 (128 -> 128 -> 64): layer 1 gathers X (mean, M written), layer 2
-    projects first and gathers the 64-wide Z (plus S); the GEMM label is the
-    mean of its two launches."""
+    """Two layers -> two launches per kernel per step: the model is the mean."""
     c = W.CONFIGS["C2"]
     n, e = c.n, c.num_edges
-    alg = bench.algorithmic(c)
-    base = e * 4 + (n + 1) * 8 + n * 4
-    assert alg["agg_mean_bf16"]["bytes"] == base + 2 * n * 128 * 2      # X read + M written
-    assert alg["agg_sage_proj_bf16"]["bytes"] == base + 3 * n * 64 * 2  # Z, S read + out written
-    assert alg["gemm_bf16_tc"]["flops"] == (2 * n * 256 * 128 + 2 * n * 128 * 128) // 2
+    a = bench.algorithmic(c)["agg_mean_bf16"]
+    one = e * 4 + (n + 1) * 8 + n * 4 + 2 * n * 128 * 2   # width 128 both layers: X read + M written
+    assert a["bytes"] == one
 
 
 def test_roofline_object(bench):
