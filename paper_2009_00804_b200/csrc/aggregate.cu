@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <algorithm>
 #include <cstdint>
 #include <type_traits>
@@ -744,12 +745,14 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     using DW = DenseWarp<U, typename Op::Val, kWinD, kRmap>;
     __shared__ DW warps[kWarpsPerBlock];
     extern __shared__ float Ws[];  // epilogue operand staged per block: fused-GEMV weight, or bias
-    griddep_launch();
     if (Wg) {
         for (int i = threadIdx.x; i < w_elems; i += blockDim.x) Ws[i] = Wg[i];
         __syncthreads();
     }
     griddep_wait();  // features / messages come from the call's previous kernel
+    // the dependent may be scheduled from here on: every earlier kernel of the
+    // call has completed (k_gcn_epi_rows relies on this to read Y unwaited)
+    griddep_launch();
     DW &W = warps[threadIdx.x >> 5];
     volatile DW &VW = W;
     const int lane = threadIdx.x & 31;
@@ -990,18 +993,24 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
 // act(dinv[v] Y[v] + b) -- a streaming pass over the listed rows (512-B row
 // slices, 16 B per lane, kU rows in flight per warp) instead of a one-edge
 // row flush each in the merge-path engine.
+//
+// Launched after the view's gather (unwaited = 1): the gather triggers its
+// dependents only after its own griddepcontrol.wait, i.e. once the GEMM has
+// completed, so this pass reads Y without waiting for the gather and its
+// blocks fill the SMs the gather's tail leaves idle (the two write disjoint
+// output rows).  unwaited = 0: the predecessor is the GEMM itself.
 template <int kAct, int NB>
 __global__ void __launch_bounds__(256) k_gcn_epi_rows(int32_t ne, const int32_t *__restrict__ erow,
                                                       const __nv_bfloat16 *__restrict__ Y,
                                                       const float *__restrict__ dinv, const float *__restrict__ bias,
-                                                      __nv_bfloat16 *__restrict__ out) {
+                                                      __nv_bfloat16 *__restrict__ out, int unwaited) {
     constexpr int kU = 8;
     griddep_launch();
     const int lane = threadIdx.x & 31;
     float b[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) b[i] = bias ? __ldg(bias + lane * NB + i) : 0.0f;
-    griddep_wait();  // Y comes from the call's GEMM
+    if (!unwaited) griddep_wait();  // Y comes from the call's GEMM
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kU; i0 < ne; i0 += nw * kU) {
         const int64_t my = i0 + lane;
@@ -1053,12 +1062,12 @@ __global__ void __launch_bounds__(256) k_gcn_epi_rows(int32_t ne, const int32_t 
 
 template <int kAct, int NB>
 cudaError_t gcn_epi_rows(const GraphDev &g, const __nv_bfloat16 *Y, const float *bias, __nv_bfloat16 *out,
-                         cudaStream_t st) {
+                         cudaStream_t st, int unwaited) {
     if (g.ne == 0) return cudaSuccess;
     const int64_t warps = ((int64_t)g.ne + 7) / 8;
     const unsigned blocks = (unsigned)std::min<int64_t>((warps + 7) / 8, (int64_t)kNumSMs * 8);
     return launch(k_gcn_epi_rows<kAct, NB>, blocks, 256, 0, st, g.ne, (const int32_t *)g.erow, Y,
-                  (const float *)g.dinv, bias, out);
+                  (const float *)g.dinv, bias, out, unwaited);
 }
 
 template <int kAct>
@@ -1119,17 +1128,24 @@ cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32
     // in the GEMM epilogue instead cost the GEMM 0.45-0.5 ms: TMA tile
     // stores write every row.)
     if (g.arow) {
-        cudaError_t e;
+        static const bool epi_first = getenv("SAGA_EPI_FIRST") != nullptr;  // A/B switch
+        cudaError_t e = cudaSuccess;
+        if (!epi_first) {
+            e = act == SAGA_ACT_RELU ? agg_sum_bf16<SAGA_ACT_RELU>(view_agg(g), Y, f, g.adinv, bias, out, ws, st)
+                                     : agg_sum_bf16<SAGA_ACT_NONE>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
+            if (e) return e;
+        }
+        const int unwaited = !epi_first && g.antasks > 0;
         if (f == 256)
-            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 8>(g, Y, bias, out, st)
-                                     : gcn_epi_rows<SAGA_ACT_NONE, 8>(g, Y, bias, out, st);
+            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 8>(g, Y, bias, out, st, unwaited)
+                                     : gcn_epi_rows<SAGA_ACT_NONE, 8>(g, Y, bias, out, st, unwaited);
         else if (f == 128)
-            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 4>(g, Y, bias, out, st)
-                                     : gcn_epi_rows<SAGA_ACT_NONE, 4>(g, Y, bias, out, st);
+            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 4>(g, Y, bias, out, st, unwaited)
+                                     : gcn_epi_rows<SAGA_ACT_NONE, 4>(g, Y, bias, out, st, unwaited);
         else
-            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 2>(g, Y, bias, out, st)
-                                     : gcn_epi_rows<SAGA_ACT_NONE, 2>(g, Y, bias, out, st);
-        if (e) return e;
+            e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 2>(g, Y, bias, out, st, unwaited)
+                                     : gcn_epi_rows<SAGA_ACT_NONE, 2>(g, Y, bias, out, st, unwaited);
+        if (e || !epi_first) return e;
         if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
         return agg_sum_bf16<SAGA_ACT_NONE>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
     }
