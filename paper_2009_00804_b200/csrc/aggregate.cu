@@ -432,6 +432,170 @@ struct GatOp {
     }
 };
 
+// C3: GAT with the softmax shift fixed per row (reading A29).  The
+// edge softmax is invariant under a per-row shift of the scores; with M_h =
+// max_u el[u,h] (the GEMM's per-CTA maxima, reduced by k_gat_maxel) every
+// score of row v is at most S_v = LeakyReLU(M_h + er[v,h]), so the weight of
+// edge u -> v is exp(LeakyReLU(el[u] + er[v]) - S_v) <= 1: no running maximum,
+// no rescaling, and a partial row state (l, a0, a1) merges by plain addition.
+// A row whose weights all underflow (sum < kGatTiny: every score of the row
+// ~69 or more below its bound) is recomputed with the online softmax by
+// gat_row_online.  Lane L owns head h = L / 4 and output columns 2L, 2L+1 (a
+// 4-byte slice of the 128-byte z row); row value: er[v, h].
+constexpr float kGatTiny = 1e-30f;
+
+// the underflow fallback: row v's in-edges from the full CSR (the aggregation
+// view's rows keep every in-edge), single-pass online softmax, ELU(acc / l)
+__device__ __forceinline__ void gat_row_online(int32_t v, int lane, const int64_t *row_ptr, const int32_t *col_src,
+                                               const __nv_bfloat16 *z, const float *el, const float *er, float slope,
+                                               __nv_bfloat16 *out) {
+    const int h = lane >> 2;
+    const float erv = __ldg(er + (int64_t)v * 8 + h);
+    float m = -INFINITY, l = 0.0f, a0 = 0.0f, a1 = 0.0f;
+    for (int64_t q = __ldg(row_ptr + v), q1 = __ldg(row_ptr + v + 1); q < q1; ++q) {
+        const int32_t u = __ldg(col_src + q);
+        float x = __ldg(el + (int64_t)u * 8 + h) + erv;
+        x = fmaxf(x, slope * x);
+        const float mn = fmaxf(m, x);
+        const float co = __expf(m - mn), pe = __expf(x - mn);
+        const float2 f = ptx::unpack_bf16x2(__ldg(reinterpret_cast<const uint32_t *>(z + (int64_t)u * 64) + lane));
+        l = l * co + pe;
+        a0 = a0 * co + pe * f.x;
+        a1 = a1 * co + pe * f.y;
+        m = mn;
+    }
+    const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+    float x0 = a0 * inv, x1 = a1 * inv;
+    x0 = x0 > 0.0f ? x0 : __expf(x0) - 1.0f;
+    x1 = x1 > 0.0f ? x1 : __expf(x1) - 1.0f;
+    reinterpret_cast<uint32_t *>(out + (int64_t)v * 64)[lane] = ptx::pack_bf16x2(x0, x1);
+}
+
+template <bool kMap>
+struct GatShiftOp {
+    static constexpr int kWin = 8;
+    static constexpr int kSlot = 128;
+    __device__ static int win_col(int lane) { return lane >> 2; }
+    // l is lane-partial: the head's 4 lanes each sum part of the weights
+    // (finish adds them up; save / merge keep the lane partials)
+    struct Acc { float l, a0, a1, S; };
+    struct alignas(8) Val { uint32_t z2; float el; };
+    const __nv_bfloat16 *z;
+    const float *el, *er;
+    const float *Mh;   // [8] max_u el[u, h]
+    float slope;
+    __nv_bfloat16 *out;
+    const int32_t *rmap;  // kMap: the aggregation view's row -> vertex
+    const int64_t *row_ptr;  // the fallback's full CSR
+    const int32_t *col_src;
+    __device__ __forceinline__ float row_value(int32_t v, int j) const {
+        const int32_t u = kMap ? __ldg(rmap + v) : v;
+        return __ldg(er + (int64_t)u * 8 + j);
+    }
+    __device__ __forceinline__ void zero(Acc &c) const { c.l = 0.f; c.a0 = 0.f; c.a1 = 0.f; }
+    // the row's shift S_v (times log2 e)
+    __device__ __forceinline__ void begin_row(Acc &c, int32_t, int lane, float er_h) const {
+        const float x = __ldg(Mh + (lane >> 2)) + er_h;
+        c.S = fmaxf(x, slope * x) * 1.4426950408889634f;
+    }
+    __device__ __forceinline__ float weight(float el_u, float er_h, float S) const {
+        const float x = el_u + er_h;
+        return ptx::exp2_ftz(fmaf(fmaxf(x, slope * x), 1.4426950408889634f, -S));  // LeakyReLU, 0 <= slope <= 1
+    }
+    __device__ __forceinline__ Val load(int32_t u, int lane) const {
+        Val v;
+        v.z2 = __ldg(reinterpret_cast<const uint32_t *>(
+            ptx::mad_wide((uint32_t)u, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
+        v.el = __ldg(reinterpret_cast<const float *>(
+            ptx::mad_wide((uint32_t)u, 32u, reinterpret_cast<const char *>(el) + (lane >> 2) * 4)));
+        return v;
+    }
+    // one edge (the parked path): lane 4h of each head adds the weight to l
+    __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h) const {
+        const float pe = weight(v.el, er_h, c.S);
+        const float2 f = ptx::unpack_bf16x2(v.z2);
+        if ((threadIdx.x & 3) == 0) c.l += pe;
+        c.a0 = fmaf(pe, f.x, c.a0);
+        c.a1 = fmaf(pe, f.y, c.a1);
+    }
+    // Grouped weights (the engine's batch hooks, U = 8): lane 4h + i loads el
+    // of edges i and i + 4 and forms their two weights; each weight is
+    // broadcast to the head's 4 lanes by a shuffle.
+    static constexpr bool kGroupScores = true;
+    struct Batch { float el1, el2; };
+    template <int U>
+    __device__ __forceinline__ void load_batch(Val (&v)[U], Batch &b, int32_t cs, int base, int lane) const {
+        static_assert(U == 8, "two edges per lane of a head's 4 lanes");
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t src = __shfl_sync(0xffffffffu, cs, base + u);
+            v[u].z2 = __ldg(reinterpret_cast<const uint32_t *>(
+                ptx::mad_wide((uint32_t)src, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
+        }
+        const int e1 = lane & 3;
+        const int32_t s1 = __shfl_sync(0xffffffffu, cs, base + e1);
+        const int32_t s2 = __shfl_sync(0xffffffffu, cs, base + e1 + 4);
+        const char *elh = reinterpret_cast<const char *>(el) + (lane >> 2) * 4;
+        b.el1 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s1, 32u, elh)));
+        b.el2 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s2, 32u, elh)));
+    }
+    template <int U>
+    __device__ __forceinline__ void add_batch_grouped(Acc &c, const Val (&v)[U], const Batch &b, float er_h,
+                                                      int lane) const {
+        const float p1 = weight(b.el1, er_h, c.S), p2 = weight(b.el2, er_h, c.S);
+        c.l += p1 + p2;
+        const int gb = lane & ~3;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float pe = __shfl_sync(0xffffffffu, u < 4 ? p1 : p2, gb | (u & 3));
+            const float2 f = ptx::unpack_bf16x2(v[u].z2);
+            c.a0 = fmaf(pe, f.x, c.a0);
+            c.a1 = fmaf(pe, f.y, c.a1);
+        }
+    }
+    // a batch leaving the fast path: every lane takes its head's el of each edge
+    template <int U>
+    __device__ __forceinline__ void unpack_batch(Val (&v)[U], const Batch &b, int lane) const {
+        const int gb = lane & ~3;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u].el = __shfl_sync(0xffffffffu, u < 4 ? b.el1 : b.el2, gb | (u & 3));
+    }
+    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
+        float l = c.l + __shfl_xor_sync(kFull, c.l, 1);
+        l += __shfl_xor_sync(kFull, l, 2);
+        if (__any_sync(kFull, l < kGatTiny)) {  // (warp-uniform: every caller runs the whole warp)
+            gat_row_online(v, lane, row_ptr, col_src, z, el, er, slope, out);
+            return;
+        }
+        const float inv = 1.0f / l;
+        float x0 = c.a0 * inv, x1 = c.a1 * inv;
+        x0 = x0 > 0.0f ? x0 : __expf(x0) - 1.0f;  // ELU; within 1e-7 absolute of expm1 (output is bf16)
+        x1 = x1 > 0.0f ? x1 : __expf(x1) - 1.0f;
+        reinterpret_cast<uint32_t *>(out + (int64_t)v * 64)[lane] = ptx::pack_bf16x2(x0, x1);
+    }
+    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
+        reinterpret_cast<float4 *>(slot)[lane] = make_float4(c.l, c.a0, c.a1, 0.0f);
+    }
+    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
+        const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot) + lane);
+        c.l += x.x;
+        c.a0 += x.y;
+        c.a1 += x.z;
+    }
+};
+
+// M_h = max over the GAT GEMM's per-CTA maxima of el (one warp)
+__global__ void __launch_bounds__(32) k_gat_maxel(const float *__restrict__ parts, int nparts, float *__restrict__ Mh) {
+    griddep_wait();  // the maxima come from the GEMM
+    const int lane = threadIdx.x;
+    float m = -INFINITY;
+    for (int i = lane >> 3; i < nparts; i += 4) m = fmaxf(m, __ldcg(parts + i * 8 + (lane & 7)));
+    m = fmaxf(m, __shfl_xor_sync(kFull, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(kFull, m, 16));
+    if (lane < 8) Mh[lane] = m;
+    griddep_launch();
+}
+
 // C4 / R-GCN: sums (or means) of fp32 rows of 128 over the graph's typed view,
 // whose rows are (destination, type) pairs r = v * T + t (graph_build.cu step
 // 7), so S[r] lands at S[v][t][:] -- one accumulator per lane, no per-edge
@@ -546,7 +710,7 @@ struct EdgeMlpOp {
 #pragma unroll
         for (int i = 0; i < 4; ++i) c.a[i] = kMax ? -INFINITY : 0.0;
     }
-    __device__ __forceinline__ void begin_row(Acc &c, int32_t v, int lane) const {
+    __device__ __forceinline__ void begin_row(Acc &c, int32_t v, int lane, float) const {
         c.hs = __ldg(hslot + v);
         c.b = __ldg(reinterpret_cast<const float4 *>(
             ptx::mad_wide((uint32_t)v, 1024u, reinterpret_cast<const char *>(AB) + 512 + lane * 16)));
@@ -657,9 +821,10 @@ struct has_begin_row { static constexpr bool value = false; };
 template <typename Op>
 struct has_begin_row<Op, decltype(void(&Op::begin_row))> { static constexpr bool value = true; };
 template <typename Op>
-__device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, int32_t v, int32_t n, int lane) {
+__device__ __forceinline__ void begin_row_of(const Op &op, typename Op::Acc &c, int32_t v, int32_t n, int lane,
+                                             float rs) {
     if constexpr (has_begin_row<Op>::value) {
-        if (v < n) op.begin_row(c, v, lane);
+        if (v < n) op.begin_row(c, v, lane, rs);
     }
 }
 
@@ -684,12 +849,12 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
     if (old == (int)(k2 - k1)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         if (lane == 0) ws.counters[k2] = 0;  // every contributor has taken its ticket: leave it zero
+        const float rs = Op::kWin ? op.row_value(r, Op::win_col(lane)) : 0.0f;
         typename Op::Acc m;
         op.zero(m);
-        begin_row_of(op, m, r, r + 1, lane);  // per-row state the epilogue may read
+        begin_row_of(op, m, r, r + 1, lane, rs);  // per-row state the epilogue may read
         op.merge(m, ws.partials + (2 * k1 + 1) * Op::kSlot, lane);
         for (int64_t kk = k1 + 1; kk <= k2; ++kk) op.merge(m, ws.partials + (2 * kk) * Op::kSlot, lane);
-        const float rs = Op::kWin ? op.row_value(r, Op::win_col(lane)) : 0.0f;
         do_finish(op, rmap ? __ldg(rmap + r) : r, m, rs, lane, Ws, 0);
     }
 }
@@ -800,7 +965,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
 
     typename Op::Acc acc;
     op.zero(acc);
-    begin_row_of(op, acc, v, g.n, lane);
+    begin_row_of(op, acc, v, g.n, lane, rs);
 
     // finish row v (or save its partial if it is the head row), advance to v+1
     auto flush = [&]() {
@@ -823,7 +988,7 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
         row_end = VW.re[v - wr];
         if (kWin) rs = VW.rv[(v - wr) * kWinD + Op::win_col(lane)];
         op.zero(acc);
-        begin_row_of(op, acc, v, g.n, lane);
+        begin_row_of(op, acc, v, g.n, lane, rs);
     };
 
     // keeps q - cb < 32; batches start at p + multiple of U and U | 32, so a
@@ -1170,16 +1335,25 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 }
 
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
-                            float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st) {
-    // with the aggregation view the GEMM epilogue has written the rows whose only
-    // in-edge is the self-loop (or with none); the rest run over the compacted CSR
-    // 48 registers, 40 warps per SM: 3% faster than 4 blocks.  With the
-    // aggregation view (the GEMM epilogue has written ELU(z) of the rows whose
-    // only in-edge is the self-loop, and 0 for rows without one) the kernel
-    // runs over the other rows only: C3 gat_edge 205 -> 183 us for +9 us of
-    // GEMM output stores.
-    if (g.arow) return run<8, 5>(view_agg_fine(g), GatOp<true>{z, el, er, slope, out, g.arow}, ws, st);
-    return run<8, 5>(view_fine(g), GatOp<false>{z, el, er, slope, out, nullptr}, ws, st);
+                            const GatSoftmaxWs &sw, float slope, __nv_bfloat16 *out, AggWorkspace ws,
+                            cudaStream_t st) {
+    // With the aggregation view (the GEMM epilogue has written ELU(z) of the
+    // rows whose only in-edge is the self-loop, and 0 for rows without one) the
+    // kernel runs over the other rows only: C3 gat_edge 205 -> 183 us for +9 us
+    // of GEMM output stores (round 1 kernel, online softmax).
+    static const bool online = getenv("SAGA_GAT_ONLINE") != nullptr;  // A/B switch
+    if (online) {
+        if (g.arow) return run<8, 5>(view_agg_fine(g), GatOp<true>{z, el, er, slope, out, g.arow}, ws, st);
+        return run<8, 5>(view_fine(g), GatOp<false>{z, el, er, slope, out, nullptr}, ws, st);
+    }
+    if (g.n == 0) return cudaSuccess;
+    cudaError_t e = launch(k_gat_maxel, 1, 32, 0, st, (const float *)sw.parts, sw.nparts, sw.Mh);
+    if (e) return e;
+    if (g.arow)
+        return run<8, 5>(view_agg_fine(g),
+                         GatShiftOp<true>{z, el, er, sw.Mh, slope, out, g.arow, g.row_ptr, g.col_src}, ws, st);
+    return run<8, 5>(view_fine(g), GatShiftOp<false>{z, el, er, sw.Mh, slope, out, nullptr, g.row_ptr, g.col_src},
+                     ws, st);
 }
 
 cudaError_t launch_agg_typed_f32(const GraphDev &g, const float *H, int32_t f, float *S, bool mean, double *Sx,

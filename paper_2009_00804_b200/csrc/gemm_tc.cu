@@ -41,6 +41,7 @@ struct alignas(8) Barriers {
     uint64_t full[8], empty[8], tfull[2], tempty[2], wready;
     uint32_t tmem_base;
     float vec[256];  // epilogue vectors staged once per CTA: bias[BN], or GAT a_src[64] | a_dst[64]
+    float red[4][8];  // GAT: the epilogue warps' maxima of el per head
 };
 
 template <int BN>
@@ -65,6 +66,7 @@ struct EpiParams {
     int act;
     const float *a_src, *a_dst;
     float *el, *er;
+    float *elmax;   // GAT: per-CTA maxima of el per head, [gridDim.x][8] (the edge softmax's shift)
     bool self_out;  // GAT: the aggregation view's output tile (GemmArgs::out2; kernel template SELF)
 };
 
@@ -247,6 +249,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         griddep_wait();  // before this grid's first global write
         int it = 0;
         uint32_t cstage = 0;
+        [[maybe_unused]] float elmx[8];
+        if constexpr (EPI == EPI_GAT) {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) elmx[h] = -INFINITY;
+        }
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
@@ -369,6 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             ptx::mbar_arrive(&bar->tempty[acc]);
             if (EPI == EPI_GAT && valid) {
+#pragma unroll
+                for (int h = 0; h < 8; ++h) elmx[h] = fmaxf(elmx[h], el[h]);
                 float4 *pe = reinterpret_cast<float4 *>(ep.el + row * 8);
                 float4 *pr = reinterpret_cast<float4 *>(ep.er + row * 8);
                 pe[0] = make_float4(el[0], el[1], el[2], el[3]);
@@ -376,6 +385,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pr[0] = make_float4(er[0], er[1], er[2], er[3]);
                 pr[1] = make_float4(er[4], er[5], er[6], er[7]);
             }
+        }
+        if constexpr (EPI == EPI_GAT) {
+            // this CTA's maximum of el per head -> ep.elmax[blockIdx.x]
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) elmx[h] = fmaxf(elmx[h], __shfl_xor_sync(0xffffffffu, elmx[h], o));
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int h = 0; h < 8; ++h) bar->red[q][h] = elmx[h];
+            }
+            named_bar(1, 128);
+            if (et < 8)
+                ep.elmax[blockIdx.x * 8 + et] =
+                    fmaxf(fmaxf(bar->red[0][et], bar->red[1][et]), fmaxf(bar->red[2][et], bar->red[3][et]));
         }
         if (et == 0) ptx::bulk_wait<0>();
     }
@@ -414,15 +439,20 @@ cudaError_t launch_bn(const GemmArgs &a, const CUtensorMap &m0, const CUtensorMa
     cudaError_t e =
         cudaFuncSetAttribute(k_gemm_bf16_tc<BN, EPI, SELF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e) return e;
-    const int64_t ntiles = (a.M + kBM - 1) / kBM;
-    int dev = 0, sms = kNumSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
+    const unsigned grid = (unsigned)gemm_bf16_tc_grid(a.M);
     return launch(k_gemm_bf16_tc<BN, EPI, SELF>, grid, kThreads, L::kBytes, st, m0, m1, mc, mo, a.W, a.M, KB, KB0, ep);
 }
 
 }  // namespace
+
+// persistent grid: one CTA per SM, at most one per 128-row tile
+int gemm_bf16_tc_grid(int64_t M) {
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+    return (int)(ntiles < sms ? ntiles : sms);
+}
 
 // 2-D bf16 row-major [rows][cols] map with a {64 col, box_rows row} box, 128B swizzle.
 bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int box_rows) {  // box_rows <= 256
@@ -439,6 +469,10 @@ bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols,
 
 cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char **why) {
     if (a.M == 0) return cudaSuccess;
+    if (a.epi == EPI_GAT && !a.elmax) {
+        *why = "GAT GEMM needs elmax";
+        return cudaErrorInvalidValue;
+    }
     const int K = a.K0 + a.K1;
     if (a.K0 % kBK || a.K1 % kBK || K > 256 || K == 0) {
         *why = "GEMM K must be a multiple of 64 and <= 256";
@@ -450,7 +484,7 @@ cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char *
         *why = "cuTensorMapEncodeTiled failed";
         return cudaErrorInvalidValue;
     }
-    EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er,
+    EpiParams ep{a.epi, a.row_scale, a.bias, a.act, a.a_src, a.a_dst, a.el, a.er, a.elmax,
                  a.epi == EPI_GAT && a.out2};
     const int KB = K / kBK, KB0 = a.K0 / kBK;
     // instantiated modes: GCN (row scale), SAGE / LSTM (bias + act), GAT (N = 64,

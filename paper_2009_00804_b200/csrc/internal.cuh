@@ -144,8 +144,16 @@ cudaError_t launch_gcn_f32_fused(const GraphDev &g, const float *X, int32_t f_in
 cudaError_t launch_agg_mean_bf16(const GraphDev &g, const __nv_bfloat16 *X, int32_t f, __nv_bfloat16 *M,
                                  AggWorkspace ws, cudaStream_t st);
 // GAT fused edge kernel: online softmax + aggregate + ELU.
+// GAT softmax shift (reading A29): the GEMM's per-CTA maxima of el and their
+// maximum per head, M_h (k_gat_maxel).
+struct GatSoftmaxWs {
+    float *parts = nullptr;  // [nparts][8], written by the GAT GEMM (GemmArgs::elmax)
+    int nparts = 0;
+    float *Mh = nullptr;     // [8]
+};
 cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const float *el, const float *er,
-                            float slope, __nv_bfloat16 *out, AggWorkspace ws, cudaStream_t st);
+                            const GatSoftmaxWs &sw, float slope, __nv_bfloat16 *out, AggWorkspace ws,
+                            cudaStream_t st);
 // GATED typed sums: S[v][t][:] = sum_{type t} H[u]  (fp32)
 // GATED / RGCN typed sums over the typed view (mean = per-type means, R-GCN):
 // S[v][t][:] for t < T (layout [n][T][f], fp32 out, fp64 accumulation); without
@@ -173,8 +181,10 @@ struct GemmArgs {
     int act = 0;
     const float *a_src = nullptr, *a_dst = nullptr;    // EPI_GAT [heads][8]
     float *el = nullptr, *er = nullptr;                // EPI_GAT [M][heads]
+    float *elmax = nullptr;  // EPI_GAT: per-CTA maxima of el per head [gemm_bf16_tc_grid(M)][heads]
 };
 cudaError_t launch_gemm_bf16_tc(const GemmArgs &a, cudaStream_t st, const char **why);
+int gemm_bf16_tc_grid(int64_t M);  // CTAs of launch_gemm_bf16_tc for M rows
 
 // Heavy rows deg_order[0 .. n_heavy) of the gated / GGNN layers (gru_f64.cu):
 // fp64 ApplyVertex -- the message GEMM from Sx [n_heavy][T][f] (gated) or m

@@ -165,6 +165,7 @@ void keep_pool_memory() {
 }
 
 constexpr size_t kAlign = 256;
+constexpr int kGatMaxParts = 1024;  // GAT: per-CTA maxima slots (the GEMM runs one CTA per SM)
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Workspace plan: [counters | partials | model intermediates].
@@ -201,7 +202,8 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
         case SAGA_GAT:
             p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0));               // z bf16
             p.inter1 = align_up(sizeof(float) * n * 8);                                         // el
-            p.inter2 = align_up(sizeof(float) * n * 8);                                         // er
+            // er, then the GEMM's per-CTA maxima of el and their maximum M_h
+            p.inter2 = align_up(sizeof(float) * (n * 8 + (size_t)kGatMaxParts * 8 + 8));
             break;
         case SAGA_GATED:
             p.inter0 = align_up(sizeof(float) * n * (size_t)g.num_etypes * (size_t)std::max(o.in_dim, 0));  // S [n][T][f]
@@ -554,13 +556,18 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
         case SAGA_GAT: {
             __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(i0);
             float *el = reinterpret_cast<float *>(i1), *er = reinterpret_cast<float *>(i2);
+            GatSoftmaxWs sw;
+            sw.parts = er + (size_t)d.n * 8;
+            sw.Mh = sw.parts + (size_t)kGatMaxParts * 8;
+            sw.nparts = gemm_bf16_tc_grid(d.n);
+            if (sw.nparts > kGatMaxParts) return fail(SAGA_EUNSUPPORTED, "GAT: more than %d SMs", kGatMaxParts);
             GemmArgs a;
             a.M = d.n; a.K0 = o.in_dim; a.K1 = 0; a.N = 64;
             a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
             a.W = static_cast<const __nv_bfloat16 *>(w->W);
             a.out = z;
             a.epi = EPI_GAT;
-            a.a_src = w->attn_src; a.a_dst = w->attn_dst; a.el = el; a.er = er;
+            a.a_src = w->attn_src; a.a_dst = w->attn_dst; a.el = el; a.er = er; a.elmax = sw.parts;
             if (d.arow) {  // the epilogue writes ELU(z) of the self-loop-only rows (aggregation view)
                 a.row_scale = d.dinv;
                 a.out2 = static_cast<__nv_bfloat16 *>(out->data);
@@ -572,7 +579,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             if (e) return fail(SAGA_ECUDA, "gat gemm: %s (%s)", cudaGetErrorString(e), why);
             {
                 ProfScope ps_("gat_edge", st);
-                e = launch_gat_edge(d, z, el, er, o.leaky_slope, static_cast<__nv_bfloat16 *>(out->data), aw, st);
+                e = launch_gat_edge(d, z, el, er, sw, o.leaky_slope, static_cast<__nv_bfloat16 *>(out->data), aw, st);
             }
             if (e) return cuda_fail(e, "gat edge");
             return SAGA_OK;

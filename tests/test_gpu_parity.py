@@ -508,3 +508,36 @@ def test_workspace_reuse_across_graphs(saga, model):
     for a, b in zip(fresh, ref):
         assert torch.equal(a, b)
     assert int(ws[:64].count_nonzero()) == 0 or model in ("gcn_f32",)  # first ticket counters left zero
+
+
+@pytest.mark.parametrize("scale", [1.0, 8.0, 40.0, 400.0])
+@pytest.mark.parametrize("hub", [0, 20000])
+def test_gat_score_range(saga, scale, hub):
+    """GAT's softmax shift per row is the bound LeakyReLU(max_u el[u] + er[v])
+    (reading A29): attention vectors scaled so the scores span a few units up
+    to thousands -- every row's weights then underflow against the bound
+    except those that reach max el, and the rows whose weight sum falls below
+    kGatTiny are recomputed by the online-softmax fallback -- on a power-law
+    graph with self-loops, optionally with a hub split across tasks."""
+    n = 3001
+    rng = np.random.default_rng(13)
+    s = rng.integers(0, n, 30000).astype(np.int32)
+    d = np.minimum(rng.zipf(1.7, 30000) - 1, n - 1).astype(np.int32)
+    if hub:
+        s = np.concatenate([s, rng.integers(0, n, hub).astype(np.int32)])
+        d = np.concatenate([d, np.full(hub, 29, np.int32)])
+    s, d = zoo.with_self_loops(n, s, d)
+    cfg = _zoo_cfg("gat", n, s.shape[0])
+    x = _zoo_inputs("gat", n, s, d, 17)
+    x["a_src"] = (x["a_src"] * scale).contiguous()
+    x["a_dst"] = (x["a_dst"] * scale).contiguous()
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, layers = H.gpu_step(saga, cfg, g, dx)
+    outs2, _ = H.gpu_step(saga, cfg, g, dx, layers)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs2[0])
+    og = H.oracle_graph(oracle, cfg, x)
+    refs = H.oracle_step(oracle, cfg, og, x)
+    H.check(outs[0], refs[0], H.TOL["bf16"], f"gat scale={scale} hub={hub}")
