@@ -176,7 +176,7 @@ struct SumBf16Op {
 // weight dinv[u] per edge, then the ApplyVertex GEMV (W staged in shared
 // memory) fused into the row flush, spread over the warp (lane L computes
 // outputs L and L + 32).
-// kRowwise (graphs whose in-degrees are all <= kRowwiseMaxDeg, one warp per
+// kRowwise (graphs whose in-degrees are all <= kEllMaxDeg, one warp per
 // row): fp32 accumulation -- a sum of <= 64 terms is within ~4e-6 of fp64,
 // and the fp32 -> fp64 conversions (XU pipe) were 12% of C1's stalls.
 template <int NPL, bool kRowwise = false>
@@ -1093,16 +1093,16 @@ cudaError_t run(const GraphView &g, const Op &op, AggWorkspace ws, cudaStream_t 
     return launch(k_segreduce<U, kMinB, Op, false>, blocks, kBlock, smem, st, g, op, ws, Wg, w_elems);
 }
 
-// Small-degree graphs (every in-degree <= kRowwiseMaxDeg): one warp per row,
-// no merge-path tasks and no split rows.  Used for C1's fused GCN layer,
-// where the merge-path engine's per-task prologue and split-row tickets
-// dominated a 12K-edge graph.
-constexpr int32_t kRowwiseMaxDeg = 64;
-
+// Small-degree graphs (every in-degree <= kEllMaxDeg): one warp per row,
+// no merge-path tasks and no split rows, edges from the graph's ELL view (a
+// row's sources at a fixed offset: one dependent load fewer than row_ptr ->
+// col_src on a cold step).  Used for C1's fused GCN layer, where the
+// merge-path engine's per-task prologue and split-row tickets dominated a
+// 12K-edge graph.
 template <int U, int kMinB, typename Op>
-__global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__restrict__ row_ptr,
-                                                         const int32_t *__restrict__ col_src, int32_t n, const Op op,
-                                                         const float *Wg, const int32_t w_elems) {
+__global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int32_t *__restrict__ ell, int32_t ell_w,
+                                                         int32_t n, const Op op, const float *Wg,
+                                                         const int32_t w_elems) {
     extern __shared__ float Ws[];
     constexpr int kWReg = Op::kWPerThread;  // W elements per thread in flight (w_elems <= kWReg * kBlock)
     const int lane = threadIdx.x & 31;
@@ -1121,12 +1121,13 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_rowwise(const int64_t *__rest
     }
     griddep_wait();
     auto gather = [&](int32_t row, typename Op::Acc &acc, float &rs) {
-        const int32_t p0 = (int32_t)__ldg(row_ptr + row), p1 = (int32_t)__ldg(row_ptr + row + 1);
         rs = op.row_value(row, 0);
         op.zero(acc);
-        for (int32_t q0 = p0; q0 < p1; q0 += 32) {
-            const int32_t cnt = min(32, p1 - q0);
-            const int32_t cs = lane < cnt ? __ldg(col_src + q0 + lane) : 0;
+        for (int32_t q0 = 0; q0 < ell_w; q0 += 32) {
+            const int32_t c = q0 + lane < ell_w ? __ldg(ell + (int64_t)row * ell_w + q0 + lane) : -1;
+            const int32_t cnt = __popc(__ballot_sync(kFull, c >= 0));  // the row's sources come first
+            const int32_t cs = c >= 0 ? c : 0;
+            if (cnt == 0) break;
             for (int j = 0; j < cnt; j += U) {
                 typename Op::Val val[U];
 #pragma unroll
@@ -1263,7 +1264,7 @@ cudaError_t gcn_f32(const GraphDev &g, const float *X, int32_t f_in, const float
         GcnF32FusedOp<NPL, true> op{X, f_in, f_out, g.dinv, bias, act, out};
         const unsigned blocks = (unsigned)((g.n + kWarpsPerBlock - 1) / kWarpsPerBlock);
         return launch(k_rowwise<8, NPL == 4 ? 2 : 3, GcnF32FusedOp<NPL, true>>, blocks, kBlock,
-                      sizeof(float) * f_in * f_out, st, g.row_ptr, g.col_src, g.n, op, W, f_in * f_out);
+                      sizeof(float) * f_in * f_out, st, (const int32_t *)g.ell, g.ell_w, g.n, op, W, f_in * f_out);
     }
     GcnF32FusedOp<NPL> op{X, f_in, f_out, g.dinv, bias, act, out};
     return run<8, NPL == 4 ? 2 : 3>(view(g), op, ws, st, W, f_in * f_out);
@@ -1380,6 +1381,6 @@ cudaError_t launch_agg_edge_mlp_f32(const GraphDev &g, const float *AB, int32_t 
     return run<4, 4>(view(g), EdgeMlpOp<false, false>{AB, m, hs, Bx, mx}, ws, st);
 }
 
-bool gcn_f32_rowwise(const GraphDev &g) { return g.max_in_deg <= kRowwiseMaxDeg; }
+bool gcn_f32_rowwise(const GraphDev &g) { return g.ell != nullptr; }
 
 }  // namespace saga

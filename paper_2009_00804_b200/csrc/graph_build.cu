@@ -237,6 +237,16 @@ __global__ void k_iota(int32_t *p, int64_t e) {
         p[i] = (int32_t)i;
 }
 
+// ell[v][i] = the i-th source of row v (CSR order), -1 past the row's end
+__global__ void k_build_ell(int64_t cells, int32_t w, const int64_t *__restrict__ row_ptr,
+                            const int32_t *__restrict__ col_src, int32_t *__restrict__ ell) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const int64_t v = c / w, i = c % w;
+    const int64_t q = row_ptr[v] + i;
+    ell[c] = q < row_ptr[v + 1] ? col_src[q] : -1;
+}
+
 __global__ void k_gather_csr(int64_t e, const int32_t *__restrict__ edge_id, const int32_t *__restrict__ src,
                              const int32_t *__restrict__ etype, int32_t *col_src, int32_t *etype_csr) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < e; p += (int64_t)gridDim.x * blockDim.x) {
@@ -483,6 +493,15 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     if (n > 0) k_norms<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, g->dinv, g->inv_deg);
     SAGA_TRY(cudaGetLastError());
 
+    // 4b. ELL view of a graph with small in-degrees (the row-wise fp32 GCN)
+    if (n > 0 && g->max_in_deg <= kEllMaxDeg) {
+        g->ell_w = std::max(4, (g->max_in_deg + 3) / 4 * 4);
+        const int64_t cells = (int64_t)n * g->ell_w;
+        SAGA_TRY(cudaMallocAsync(&g->ell, sizeof(int32_t) * (size_t)cells, st));
+        k_build_ell<<<grid_for(cells, 256), 256, 0, st>>>(cells, g->ell_w, g->row_ptr, g->col_src, g->ell);
+        SAGA_TRY(cudaGetLastError());
+    }
+
     // 5. vertices by in-degree, descending (ties by id): the LSTM gather's
     //    work queue (longest sequences first)
     SAGA_TRY(cudaMallocAsync(&g->deg_order, sizeof(int32_t) * nn, st));
@@ -608,7 +627,7 @@ void free_graph(GraphDev *g) {
     void *ptrs[] = {g->row_ptr,  g->col_src,  g->edge_id,  g->etype,   g->in_deg,  g->out_deg, g->dinv,
                     g->inv_deg,  g->task_v,   g->task_p,   g->deg_order, g->heavy_slot, g->arow, g->arow_ptr,
                     g->acol_src, g->adinv, g->aftask_v, g->aftask_p, g->trow_ptr, g->tcol_src, g->tinv_deg,
-                    g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p, g->atask_v, g->atask_p, g->erow};
+                    g->ttask_v, g->ttask_p, g->ftask_v, g->ftask_p, g->atask_v, g->atask_p, g->erow, g->ell};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, st);
 }

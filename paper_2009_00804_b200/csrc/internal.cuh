@@ -15,6 +15,9 @@ constexpr int kNumSMs = 148;
 // Rows whose in-degree reaches this run the gated / GGNN ApplyVertex in fp64
 // (gru_f64.cu): their summed message outgrows the tensor core's fp32 accumulator.
 constexpr int32_t kHeavyInDeg = 256;
+// Graphs whose in-degrees are all <= this get the ELL view (graph_build.cu)
+// and the row-wise fused fp32 GCN (aggregate.cu)
+constexpr int32_t kEllMaxDeg = 64;
 
 // ---- Programmatic dependent launch (PDL) ----------------------------------
 // Inside one saga_layer call every kernel after the first is launched with
@@ -114,6 +117,11 @@ struct GraphDev {
     int64_t *atask_p = nullptr;
     int32_t ne = 0;               // host: the other rows (self-loop only, or no in-edge): n - an
     int32_t *erow = nullptr;      // [ne]  their vertices, ascending
+    // ELL view (built when every in-degree is <= kEllMaxDeg): row v's sources
+    // at ell[v * ell_w ..], CSR order, padded with -1 -- the row-wise kernels
+    // find a row's edges without the row_ptr round trip
+    int32_t ell_w = 0;            // host: width (max in-degree rounded up to 4; 0: no view)
+    int32_t *ell = nullptr;       // [n][ell_w]
     cudaStream_t stream = nullptr;  // stream the graph was built on (for saga_free)
 };
 
