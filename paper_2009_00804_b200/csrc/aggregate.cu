@@ -37,7 +37,6 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
-#include <cstdlib>
 #include <algorithm>
 #include <cstdint>
 #include <type_traits>
@@ -274,161 +273,6 @@ struct GcnF32FusedOp {
     __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
 #pragma unroll
         for (int i = 0; i < NPL; ++i) c.a[i] += (AccT)__ldcg(reinterpret_cast<const double *>(slot) + lane * NPL + i);
-    }
-};
-
-// C3: GAT.  Lane L owns head h = L / 4 and output columns 2L, 2L+1 (a 4-byte
-// slice of the 128-byte z row).  Per edge s = LeakyReLU(el[u,h] + er[v,h])
-// (the additive form of a^T [z_u || z_v], reading A14) and a single-exp
-// online-softmax update: with d = s - m, e = exp(-|d|); if d > 0 the state is
-// rescaled by e and the new term weighs 1, else the new term weighs e.
-// Flush: ELU(acc / l).  Row value: er[v, h] (kWin = 8 heads).
-template <bool kMap>
-struct GatOp {
-    static constexpr int kWin = 8;
-    static constexpr int kSlot = 128;
-    __device__ static int win_col(int lane) { return lane >> 2; }
-    struct Acc { float m, l, a0, a1; };
-    struct alignas(8) Val { uint32_t z2; float el; };
-    const __nv_bfloat16 *z;
-    const float *el, *er;
-    float slope;
-    __nv_bfloat16 *out;
-    const int32_t *rmap;  // kMap: the aggregation view's row -> vertex
-    __device__ __forceinline__ float row_value(int32_t v, int j) const {
-        const int32_t u = kMap ? __ldg(rmap + v) : v;
-        return __ldg(er + (int64_t)u * 8 + j);
-    }
-    __device__ __forceinline__ void zero(Acc &c) const { c.m = -INFINITY; c.l = 0.f; c.a0 = 0.f; c.a1 = 0.f; }
-    __device__ __forceinline__ Val load(int32_t u, int lane) const {
-        Val v;
-        v.z2 = __ldg(reinterpret_cast<const uint32_t *>(
-            ptx::mad_wide((uint32_t)u, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
-        v.el = __ldg(reinterpret_cast<const float *>(
-            ptx::mad_wide((uint32_t)u, 32u, reinterpret_cast<const char *>(el) + (lane >> 2) * 4)));
-        return v;
-    }
-    // A whole batch of one row (the engine's fast path): one rescale of the
-    // state by the batch maximum, then exp(s - m) per edge -- 1 MUFU and no
-    // selects per edge instead of the single-edge online update.
-    static constexpr bool kBatchAdd = true;
-    template <int U>
-    __device__ __forceinline__ void add_batch(Acc &c, const Val (&v)[U], float er_h) const {
-        constexpr float kLog2e = 1.4426950408889634f;
-        float s[U];
-        float mb = c.m;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float x = v[u].el + er_h;
-            s[u] = fmaxf(x, slope * x);  // LeakyReLU, 0 <= slope <= 1
-            mb = fmaxf(mb, s[u]);
-        }
-        const float ml = mb * kLog2e;
-        const float co = ptx::exp2_ftz(fmaf(c.m, kLog2e, -ml));  // 0 when c.m = -inf
-        c.l *= co;
-        c.a0 *= co;
-        c.a1 *= co;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float pe = ptx::exp2_ftz(fmaf(s[u], kLog2e, -ml));
-            const float2 f = ptx::unpack_bf16x2(v[u].z2);
-            c.l += pe;
-            c.a0 = fmaf(pe, f.x, c.a0);
-            c.a1 = fmaf(pe, f.y, c.a1);
-        }
-        c.m = mb;
-    }
-    // Grouped scores (the engine's batch hooks, U = 8): a head's 4 lanes
-    // compute its 8 edge scores two each -- lane 4h + i takes edges i and
-    // i + 4 -- instead of all 8 in every lane, so a batch loads 2 el values
-    // and runs 2 exps per lane instead of 8; the batch max is a 4-lane
-    // reduction and each exp is broadcast to the head's lanes by a shuffle.
-    // Same values in the same order as add_batch (bit-identical).
-    static constexpr bool kGroupScores = true;
-    struct Batch { float el1, el2; };
-    template <int U>
-    __device__ __forceinline__ void load_batch(Val (&v)[U], Batch &b, int32_t cs, int base, int lane) const {
-        static_assert(U == 8, "two edges per lane of a head's 4 lanes");
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t src = __shfl_sync(0xffffffffu, cs, base + u);
-            v[u].z2 = __ldg(reinterpret_cast<const uint32_t *>(
-                ptx::mad_wide((uint32_t)src, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
-        }
-        const int e1 = lane & 3;
-        const int32_t s1 = __shfl_sync(0xffffffffu, cs, base + e1);
-        const int32_t s2 = __shfl_sync(0xffffffffu, cs, base + e1 + 4);
-        const char *elh = reinterpret_cast<const char *>(el) + (lane >> 2) * 4;
-        b.el1 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s1, 32u, elh)));
-        b.el2 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s2, 32u, elh)));
-    }
-    template <int U>
-    __device__ __forceinline__ void add_batch_grouped(Acc &c, const Val (&v)[U], const Batch &b, float er_h,
-                                                      int lane) const {
-        constexpr float kLog2e = 1.4426950408889634f;
-        const float x1 = b.el1 + er_h, x2 = b.el2 + er_h;
-        const float s1 = fmaxf(x1, slope * x1), s2 = fmaxf(x2, slope * x2);  // LeakyReLU, 0 <= slope <= 1
-        float mb = fmaxf(s1, s2);
-        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
-        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
-        mb = fmaxf(mb, c.m);
-        const float ml = mb * kLog2e;
-        const float co = ptx::exp2_ftz(fmaf(c.m, kLog2e, -ml));  // 0 when c.m = -inf
-        c.l *= co;
-        c.a0 *= co;
-        c.a1 *= co;
-        const float p1 = ptx::exp2_ftz(fmaf(s1, kLog2e, -ml)), p2 = ptx::exp2_ftz(fmaf(s2, kLog2e, -ml));
-        const int gb = lane & ~3;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float pe = __shfl_sync(0xffffffffu, u < 4 ? p1 : p2, gb | (u & 3));
-            const float2 f = ptx::unpack_bf16x2(v[u].z2);
-            c.l += pe;
-            c.a0 = fmaf(pe, f.x, c.a0);
-            c.a1 = fmaf(pe, f.y, c.a1);
-        }
-        c.m = mb;
-    }
-    // a batch leaving the fast path: every lane takes its head's el of each edge
-    template <int U>
-    __device__ __forceinline__ void unpack_batch(Val (&v)[U], const Batch &b, int lane) const {
-        const int gb = lane & ~3;
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u].el = __shfl_sync(0xffffffffu, u < 4 ? b.el1 : b.el2, gb | (u & 3));
-    }
-    __device__ __forceinline__ void add(Acc &c, const Val &v, float er_h) const {
-        float s = v.el + er_h;
-        s = fmaxf(s, slope * s);                 // LeakyReLU for 0 <= slope <= 1
-        const float d = s - c.m;                 // +inf for the first term
-        const float e = ptx::exp2_ftz(-fabsf(d) * 1.4426950408889634f);  // exp(-|d|); 0 for the first term
-        const bool up = d > 0.0f;
-        const float co = up ? e : 1.0f, cn = up ? 1.0f : e;
-        const float2 f = ptx::unpack_bf16x2(v.z2);
-        c.l = fmaf(c.l, co, cn);
-        c.a0 = fmaf(c.a0, co, cn * f.x);
-        c.a1 = fmaf(c.a1, co, cn * f.y);
-        c.m = up ? s : c.m;
-    }
-    __device__ __forceinline__ void finish(int32_t v, const Acc &c, float, int lane, const float *) const {
-        const float inv = c.l > 0.0f ? 1.0f / c.l : 0.0f;
-        float x0 = c.a0 * inv, x1 = c.a1 * inv;
-        x0 = x0 > 0.0f ? x0 : __expf(x0) - 1.0f;  // ELU; within 1e-7 absolute of expm1 (output is bf16)
-        x1 = x1 > 0.0f ? x1 : __expf(x1) - 1.0f;
-        reinterpret_cast<uint32_t *>(out + (int64_t)v * 64)[lane] = ptx::pack_bf16x2(x0, x1);
-    }
-    __device__ __forceinline__ void save(float *slot, const Acc &c, int lane) const {
-        reinterpret_cast<float4 *>(slot)[lane] = make_float4(c.m, c.l, c.a0, c.a1);
-    }
-    // flash-decoding merge of another partial (m, l, a0, a1)
-    __device__ __forceinline__ void merge(Acc &c, const float *slot, int lane) const {
-        const float4 x = __ldcg(reinterpret_cast<const float4 *>(slot) + lane);
-        const float mn = fmaxf(c.m, x.x);
-        if (mn == -INFINITY) return;  // both empty
-        const float co = __expf(c.m - mn), cp = __expf(x.x - mn);
-        c.l = c.l * co + x.y * cp;
-        c.a0 = c.a0 * co + x.z * cp;
-        c.a1 = c.a1 * co + x.w * cp;
-        c.m = mn;
     }
 };
 
@@ -859,14 +703,14 @@ __device__ __noinline__ void ticket_merge(const Op &op, AggWorkspace ws, int64_t
     }
 }
 
-// Ops with a batch-level fast-path update (GAT) declare kBatchAdd.
+// Ops with a batch-level fast-path update declare kBatchAdd.
 template <typename Op, typename = void>
 struct has_batch_add { static constexpr bool value = false; };
 template <typename Op>
 struct has_batch_add<Op, decltype(void(Op::kBatchAdd))> { static constexpr bool value = Op::kBatchAdd; };
 
 // Ops whose batch loads and scores are shared across lanes declare kGroupScores
-// (GatOp: load_batch / add_batch_grouped / unpack_batch and a Batch type).
+// (GatShiftOp: load_batch / add_batch_grouped / unpack_batch and a Batch type).
 template <typename Op, typename = void>
 struct has_group_scores { static constexpr bool value = false; };
 template <typename Op>
@@ -1290,18 +1134,16 @@ cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32
     // Rows whose only in-edge is the self-loop (52% of C5's) go through a
     // streaming pass; the engine runs over the aggregation view of the rest.
     // C5, ncu: 0.36 ms (2.2 GB at 6.1 TB/s) + 2.65 ms, against 3.09 ms for the
-    // engine over every row; in-step 3.80 -> 3.70 ms.  (Finishing those rows
-    // in the GEMM epilogue instead cost the GEMM 0.45-0.5 ms: TMA tile
-    // stores write every row.)
+    // engine over every row; in-step 3.80 -> 3.70 ms.  The pass runs after
+    // the gather and fills its tail (3.73-3.75 -> 3.61 ms with the pass
+    // first).  (Finishing those rows in the GEMM epilogue instead cost the
+    // GEMM 0.45-0.5 ms: TMA tile stores write every row.)
     if (g.arow) {
-        static const bool epi_first = getenv("SAGA_EPI_FIRST") != nullptr;  // A/B switch
-        cudaError_t e = cudaSuccess;
-        if (!epi_first) {
-            e = act == SAGA_ACT_RELU ? agg_sum_bf16<SAGA_ACT_RELU>(view_agg(g), Y, f, g.adinv, bias, out, ws, st)
-                                     : agg_sum_bf16<SAGA_ACT_NONE>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
-            if (e) return e;
-        }
-        const int unwaited = !epi_first && g.antasks > 0;
+        cudaError_t e = act == SAGA_ACT_RELU
+                            ? agg_sum_bf16<SAGA_ACT_RELU>(view_agg(g), Y, f, g.adinv, bias, out, ws, st)
+                            : agg_sum_bf16<SAGA_ACT_NONE>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
+        if (e) return e;
+        const int unwaited = g.antasks > 0;
         if (f == 256)
             e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 8>(g, Y, bias, out, st, unwaited)
                                      : gcn_epi_rows<SAGA_ACT_NONE, 8>(g, Y, bias, out, st, unwaited);
@@ -1311,9 +1153,7 @@ cudaError_t launch_agg_gcn_bf16(const GraphDev &g, const __nv_bfloat16 *Y, int32
         else
             e = act == SAGA_ACT_RELU ? gcn_epi_rows<SAGA_ACT_RELU, 2>(g, Y, bias, out, st, unwaited)
                                      : gcn_epi_rows<SAGA_ACT_NONE, 2>(g, Y, bias, out, st, unwaited);
-        if (e || !epi_first) return e;
-        if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
-        return agg_sum_bf16<SAGA_ACT_NONE>(view_agg(g), Y, f, g.adinv, bias, out, ws, st);
+        return e;
     }
     if (act == SAGA_ACT_RELU) return agg_sum_bf16<SAGA_ACT_RELU>(view(g), Y, f, g.dinv, bias, out, ws, st);
     return agg_sum_bf16<SAGA_ACT_NONE>(view(g), Y, f, g.dinv, bias, out, ws, st);
@@ -1342,11 +1182,6 @@ cudaError_t launch_gat_edge(const GraphDev &g, const __nv_bfloat16 *z, const flo
     // rows whose only in-edge is the self-loop, and 0 for rows without one) the
     // kernel runs over the other rows only: C3 gat_edge 205 -> 183 us for +9 us
     // of GEMM output stores (round 1 kernel, online softmax).
-    static const bool online = getenv("SAGA_GAT_ONLINE") != nullptr;  // A/B switch
-    if (online) {
-        if (g.arow) return run<8, 5>(view_agg_fine(g), GatOp<true>{z, el, er, slope, out, g.arow}, ws, st);
-        return run<8, 5>(view_fine(g), GatOp<false>{z, el, er, slope, out, nullptr}, ws, st);
-    }
     if (g.n == 0) return cudaSuccess;
     cudaError_t e = launch(k_gat_maxel, 1, 32, 0, st, (const float *)sw.parts, sw.nparts, sw.Mh);
     if (e) return e;

@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_launch.log 2>&1
 for c in C5 C3 C4 C2 C1 C6 C7 C8; do
   timeout 300 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/plain_$c.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_gcn_epi|k_split' -s 3 -c 9 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_gcn_epi|k_split|k_gat_maxel' -s 3 -c 9 \
       -o gpurun_out/$TAG/full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_full_$c.log 2>&1
 done
 ls gpurun_out/$TAG

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)]
     "C1": [("GcnF32FusedOp", "gcn_f32_fused")],
     "C2": [("SumBf16Op", "agg_mean_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
-    "C3": [("GatOp", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
+    "C3": [("GatShiftOp", "gat_edge"), ("k_gat_maxel", "gat_edge"), ("k_gemm_bf16_tc", "gemm_bf16_tc_gat")],
     "C4": [("SumF32Op", "agg_typed_f32"), ("k_gemm_tf32split", "gated_apply_tf32x3"), ("k_split_weights", "gated_apply_tf32x3"),
            ("k_gru_heavy_f64", "gru_heavy_f64")],
     "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gcn_epi_rows", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
