@@ -752,7 +752,7 @@ def run_e2e(args, cfg, saga, H, d, dev, ws):
             fe = torch.cuda.Event()
             fe.record(s_out)
             out_free[sl] = fe
-        g.close()
+        g.close(sync=False)  # built and used on `main` only: a stream-ordered free, no host wait
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     d2h = host_out[0].numel() * host_out[0].element_size()

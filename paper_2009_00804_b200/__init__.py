@@ -178,11 +178,15 @@ class Graph:
         self.handle = handle
         self.num_vertices, self.num_edges, self.num_etypes = n, e, t
 
-    def close(self):
+    def close(self, sync=True):
         """saga_free is stream-ordered on the BUILD stream only (saga.h): layers
-        may have used the graph on other streams, so wait for the device first."""
+        may have used the graph on other streams, so wait for the device first.
+        sync=False skips that wait: for a graph used only on its build stream
+        (a serving loop on one stream), the stream-ordered free already follows
+        every use, and the host does not block."""
         if self.handle:
-            torch.cuda.synchronize()
+            if sync:
+                torch.cuda.synchronize()
             saga_free(self)
             self.handle = None
 

@@ -541,3 +541,21 @@ def test_gat_score_range(saga, scale, hub):
     og = H.oracle_graph(oracle, cfg, x)
     refs = H.oracle_step(oracle, cfg, og, x)
     H.check(outs[0], refs[0], H.TOL["bf16"], f"gat scale={scale} hub={hub}")
+
+
+def test_graph_close_stream_ordered(saga):
+    """Graph.close(sync=False): the stream-ordered free of a graph used only on
+    its build stream (bench.py's serving loop) -- graphs built, used and
+    freed back to back on one stream without a host wait give the same
+    outputs as the first one."""
+    cfg = W.scaled(W.CONFIGS["C3"], 3000, 40000, "close")
+    d = W.make_inputs(cfg, DEV)
+    outs = []
+    for _ in range(4):
+        g = H.gpu_graph(saga, cfg, d)
+        y = H.gpu_step(saga, cfg, g, d)[0][0]
+        g.close(sync=False)
+        outs.append(y)
+    torch.cuda.synchronize()
+    for y in outs[1:]:
+        assert torch.equal(y, outs[0])
