@@ -267,6 +267,8 @@ saga_status validate(saga_model kind, const saga::GraphDev &d, const saga_tensor
             if (o.act != SAGA_ACT_ELU) return fail(SAGA_EUNSUPPORTED, "GAT act must be ELU");
             if (!(o.leaky_slope >= 0.0f && o.leaky_slope <= 1.0f))
                 return fail(SAGA_EUNSUPPORTED, "GAT leaky_slope must lie in [0, 1]");
+            if (saga::gemm_bf16_tc_grid(d.n) > kGatMaxParts)  // the GEMM's per-CTA maxima slots (one CTA per SM)
+                return fail(SAGA_EUNSUPPORTED, "GAT: more than %d SMs", kGatMaxParts);
             return SAGA_OK;
         case SAGA_GATED:
             if (x->dtype != SAGA_F32) return fail(SAGA_EDTYPE, "GATED supports F32 features");
@@ -559,8 +561,7 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
             GatSoftmaxWs sw;
             sw.parts = er + (size_t)d.n * 8;
             sw.Mh = sw.parts + (size_t)kGatMaxParts * 8;
-            sw.nparts = gemm_bf16_tc_grid(d.n);
-            if (sw.nparts > kGatMaxParts) return fail(SAGA_EUNSUPPORTED, "GAT: more than %d SMs", kGatMaxParts);
+            sw.nparts = gemm_bf16_tc_grid(d.n);  // <= kGatMaxParts (validate)
             GemmArgs a;
             a.M = d.n; a.K0 = o.in_dim; a.K1 = 0; a.N = 64;
             a.A0 = static_cast<const __nv_bfloat16 *>(x->data);
