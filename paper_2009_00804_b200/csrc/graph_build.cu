@@ -429,9 +429,10 @@ __global__ void k_compact_edges(int32_t an, const int32_t *__restrict__ arow, co
     }
 }
 
-__global__ void k_degree_desc_keys(int32_t n, const int32_t *__restrict__ in_deg, int32_t *keys) {
+// keys max_deg - in_deg: ascending keys = descending degree, in bit_length(max_deg) bits
+__global__ void k_degree_desc_keys(int32_t n, const int32_t *__restrict__ in_deg, int32_t max_deg, int32_t *keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = 0x7FFFFFFF - in_deg[i];
+        keys[i] = max_deg - in_deg[i];
 }
 
 saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t *dst, const int32_t *etype,
@@ -508,9 +509,11 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     if (n > 0) {
         int32_t *keys;
         SAGA_TRY(cudaMallocAsync(&keys, sizeof(int32_t) * nn, st));
-        k_degree_desc_keys<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, keys);
+        k_degree_desc_keys<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, g->max_in_deg, keys);
         SAGA_TRY(cudaGetLastError());
-        SAGA_TRY(radix_sort_index(keys, n, 31, g->deg_order, st));
+        int kbits = 0;
+        while (kbits < 31 && (int64_t(1) << kbits) <= (int64_t)g->max_in_deg) ++kbits;  // keys <= max_deg < 2^kbits
+        SAGA_TRY(radix_sort_index(keys, n, kbits, g->deg_order, st));
         cudaFreeAsync(keys, st);
     }
     // heavy rows (in-degree >= kHeavyInDeg): the fp64 ApplyVertex of the gated / GGNN layers
