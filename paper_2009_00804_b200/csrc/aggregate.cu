@@ -847,10 +847,13 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
     };
 
     while (v < v1 && row_end <= p) flush();  // rows that end before the first edge
+    // cs_a is kept rotated so that lane 0 holds edge q's source: every
+    // shuffle of a batch takes an immediate lane, and one shfl.down per batch
+    // replaces the U per-edge lane-index adds
     int32_t q = p;
     for (; q + U <= p1; q += U) {
         slide(q);
-        const int base = q - cb;
+        constexpr int base = 0;
         typename Op::Val val[U];
         [[maybe_unused]] typename BatchOf<Op>::type bt;
         if constexpr (kGroup) {
@@ -908,12 +911,13 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_segreduce(const GraphView g, 
                 while (v < v1 && row_end == q + u + 1) flush();
             }
         }
+        cs_a = __shfl_down_sync(kFull, cs_a, U);
     }
     for (; q < p1; ++q) {  // remainder, one edge at a time
         slide(q);
-        const int idx = q - cb;
-        op.add(acc, op.load(__shfl_sync(kFull, cs_a, idx), lane), rs);
+        op.add(acc, op.load(__shfl_sync(kFull, cs_a, 0), lane), rs);
         while (v < v1 && row_end == q + 1) flush();
+        cs_a = __shfl_down_sync(kFull, cs_a, 1);
     }
     while (v < v1) flush();
     const int32_t row_beg = (v == v0) ? head_beg : (v < g.n ? (int32_t)__ldg(g.row_ptr + v) : g.e);
