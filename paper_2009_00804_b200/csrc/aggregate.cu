@@ -370,18 +370,19 @@ struct GatShiftOp {
     template <int U>
     __device__ __forceinline__ void load_batch(Val (&v)[U], Batch &b, int32_t cs, int base, int lane) const {
         static_assert(U == 8, "two edges per lane of a head's 4 lanes");
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t src = __shfl_sync(0xffffffffu, cs, base + u);
-            v[u].z2 = __ldg(reinterpret_cast<const uint32_t *>(
-                ptx::mad_wide((uint32_t)src, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
-        }
+        // el first: the weights are formed while the z rows are in flight
         const int e1 = lane & 3;
         const int32_t s1 = __shfl_sync(0xffffffffu, cs, base + e1);
         const int32_t s2 = __shfl_sync(0xffffffffu, cs, base + e1 + 4);
         const char *elh = reinterpret_cast<const char *>(el) + (lane >> 2) * 4;
         b.el1 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s1, 32u, elh)));
         b.el2 = __ldg(reinterpret_cast<const float *>(ptx::mad_wide((uint32_t)s2, 32u, elh)));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t src = __shfl_sync(0xffffffffu, cs, base + u);
+            v[u].z2 = __ldg(reinterpret_cast<const uint32_t *>(
+                ptx::mad_wide((uint32_t)src, 128u, reinterpret_cast<const char *>(z) + lane * 4)));
+        }
     }
     template <int U>
     __device__ __forceinline__ void add_batch_grouped(Acc &c, const Val (&v)[U], const Batch &b, float er_h,
