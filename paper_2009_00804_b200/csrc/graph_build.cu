@@ -494,9 +494,11 @@ saga_status build_graph(int32_t n, int64_t e, const int32_t *src, const int32_t 
     if (n > 0) k_norms<<<grid_for(n, 256), 256, 0, st>>>(n, g->in_deg, g->dinv, g->inv_deg);
     SAGA_TRY(cudaGetLastError());
 
-    // 4b. ELL view of a graph with small in-degrees (the row-wise fp32 GCN)
-    if (n > 0 && g->max_in_deg <= kEllMaxDeg) {
-        g->ell_w = std::max(4, (g->max_in_deg + 3) / 4 * 4);
+    // 4b. ELL view of a graph with small in-degrees (the row-wise fp32 GCN),
+    //     when its padding stays bounded (at most 4 E cells, or 1M)
+    const int32_t ell_w = std::max(4, (g->max_in_deg + 3) / 4 * 4);
+    if (n > 0 && g->max_in_deg <= kEllMaxDeg && (int64_t)n * ell_w <= std::max<int64_t>(4 * e, 1 << 20)) {
+        g->ell_w = ell_w;
         const int64_t cells = (int64_t)n * g->ell_w;
         SAGA_TRY(cudaMallocAsync(&g->ell, sizeof(int32_t) * (size_t)cells, st));
         k_build_ell<<<grid_for(cells, 256), 256, 0, st>>>(cells, g->ell_w, g->row_ptr, g->col_src, g->ell);

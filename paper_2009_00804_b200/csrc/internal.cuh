@@ -117,7 +117,8 @@ struct GraphDev {
     int64_t *atask_p = nullptr;
     int32_t ne = 0;               // host: the other rows (self-loop only, or no in-edge): n - an
     int32_t *erow = nullptr;      // [ne]  their vertices, ascending
-    // ELL view (built when every in-degree is <= kEllMaxDeg): row v's sources
+    // ELL view (built when every in-degree is <= kEllMaxDeg and the padded
+    // array holds at most max(4 E, 1M) cells): row v's sources
     // at ell[v * ell_w ..], CSR order, padded with -1 -- the row-wise kernels
     // find a row's edges without the row_ptr round trip
     int32_t ell_w = 0;            // host: width (max in-degree rounded up to 4; 0: no view)
