@@ -387,10 +387,11 @@ def test_random_graphs(saga, model, seed):
         H.check(y, ref, tol, f"{model}/seed {seed} (n={n}, e={s.shape[0]})/layer{i}")
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C8"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C7", "C8"])
 def test_cuda_graph_replay_matches_eager(saga, cfg):
     """bench.py times the step captured in a CUDA graph: the replayed step is
-    bit-identical to the eagerly launched one (same kernels, deterministic)."""
+    bit-identical to the eagerly launched one (same kernels, deterministic;
+    C7 also forks its batches onto the library stream inside the capture)."""
     c = W.CONFIGS[cfg]
     if c.n > 200000:
         c = W.scaled(c, 20000, 200000, cfg + "g")
