@@ -10,7 +10,7 @@
 // the recurrent GEMV h . W_hh.  Two bounds meet (C7: 1.05M steps; one hub
 // of 6,614 dependent steps): the per-SM step count and the longest chain, so
 // the work is split by sequence length (the graph's deg_order, descending):
-//   * k_lstm_pair -- sequences of >= kLongDeg steps, each on a 2-CTA
+//   * k_lstm_cluster -- sequences of >= kLongDeg steps, each on a 2-CTA
 //     cluster: CTA r owns 64 units, thread (unit, gate) with its W_hh^T row
 //     in 64 registers (128 FHFMA.BF16 per step), and the two halves of h are
 //     exchanged every step through distributed shared memory (st.async +
@@ -93,23 +93,28 @@ __device__ __forceinline__ uint32_t map_peer(uint32_t local_addr, uint32_t peer)
     return r;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    k_lstm_pair(int32_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_src,
-                const int32_t *__restrict__ order, const __nv_bfloat16 *__restrict__ P,  // [4][n][kF]
-                const uint4 *__restrict__ wt,                                            // staged W_hh^T
-                const float *__restrict__ b_ih, const float *__restrict__ b_hh,          // [4][kF]
-                __nv_bfloat16 *__restrict__ h_out, int32_t *queue, int32_t min_deg) {
+// CS CTAs per sequence (2 or 4; the cluster shape is given at launch)
+template <int CS>
+__global__ void __launch_bounds__(512 / CS, 1)
+    k_lstm_cluster(int32_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_src,
+                   const int32_t *__restrict__ order, const __nv_bfloat16 *__restrict__ P,  // [4][n][kF]
+                   const uint4 *__restrict__ wt,                                            // staged W_hh^T
+                   const float *__restrict__ b_ih, const float *__restrict__ b_hh,          // [4][kF]
+                   __nv_bfloat16 *__restrict__ h_out, int32_t *queue, int32_t min_deg) {
+    constexpr int kU = kF / CS;                  // units per CTA
+    constexpr uint32_t kPeerBytes = (CS - 1) * kU * 2;  // h bytes arriving from the other CTAs per step
     __shared__ PairSmem S;
-    const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+    const uint32_t rank = cluster_ctarank();
     const int jl = threadIdx.x / 4, g = threadIdx.x % 4;  // local unit, gate
-    const int j = 64 * (int)rank + jl;
+    const int j = kU * (int)rank + jl;
     const int lane = threadIdx.x & 31, gbase = lane & ~3, warp = threadIdx.x >> 5;
+    const int chunk = (kU / 8) * (int)rank + warp;  // this warp's 8 units: 16 bytes of hb
     if (threadIdx.x == 0) {
         ptx::mbar_init(&S.hfull[0], 1);
         ptx::mbar_init(&S.hfull[1], 1);
         ptx::fence_mbar_init();
-        ptx::mbar_arrive_expect_tx(&S.hfull[0], 64 * 2);  // armed: each phase takes the peer's 64 units
-        ptx::mbar_arrive_expect_tx(&S.hfull[1], 64 * 2);
+        ptx::mbar_arrive_expect_tx(&S.hfull[0], kPeerBytes);  // armed: each phase takes the other CTAs' units
+        ptx::mbar_arrive_expect_tx(&S.hfull[1], kPeerBytes);
     }
     griddep_wait();  // P, W_hh^T and the queue head come from the call's earlier kernels
     uint4 w[kF / 8];
@@ -118,23 +123,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const float bias = __ldg(b_ih + g * kF + j) + __ldg(b_hh + g * kF + j);
     const float ks = g == 2 ? 2.0f : 1.0f;
     const __nv_bfloat16 *Pg = P + g * (int64_t)n * kF + j;
-    // the peer's copy of this warp's 16-byte chunk of hb[b] and its mbarrier
-    const uint32_t rh0 = map_peer(ptx::smem_u32(&S.hb[0][8 * (int)rank + warp]), peer);
-    const uint32_t rh1 = map_peer(ptx::smem_u32(&S.hb[1][8 * (int)rank + warp]), peer);
-    const uint32_t rb0 = map_peer(ptx::smem_u32(&S.hfull[0]), peer);
-    const uint32_t rb1 = map_peer(ptx::smem_u32(&S.hfull[1]), peer);
+    // the other CTAs' copies of this warp's chunk of hb[b] and their mbarriers
+    uint32_t rh[2][CS - 1], rb[2][CS - 1];
+#pragma unroll
+    for (int q = 0; q < CS - 1; ++q) {
+        const uint32_t pr = (rank + 1 + q) % CS;
+        rh[0][q] = map_peer(ptx::smem_u32(&S.hb[0][chunk]), pr);
+        rh[1][q] = map_peer(ptx::smem_u32(&S.hb[1][chunk]), pr);
+        rb[0][q] = map_peer(ptx::smem_u32(&S.hfull[0]), pr);
+        rb[1][q] = map_peer(ptx::smem_u32(&S.hfull[1]), pr);
+    }
     uint32_t par[2] = {0u, 0u};
-    cluster_sync_all();  // both CTAs' barriers are initialised before any remote arrival
+    cluster_sync_all();  // every CTA's barriers are initialised before any remote arrival
     for (;;) {
         if (rank == 0 && threadIdx.x == 0) {
             const int32_t qi = atomicAdd(queue, 1);
             int32_t vv = qi < n ? order[qi] : -1;
             if (vv >= 0 && row_ptr[vv + 1] - row_ptr[vv] < min_deg) vv = -1;
             S.v = vv;
-            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_peer(ptx::smem_u32(&S.v), 1u)), "r"(vv)
-                         : "memory");
+#pragma unroll
+            for (int q = 1; q < CS; ++q)
+                asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_peer(ptx::smem_u32(&S.v), (uint32_t)q)),
+                             "r"(vv)
+                             : "memory");
         }
-        if (threadIdx.x < kF / 8) S.hb[1][threadIdx.x] = make_uint4(0, 0, 0, 0);  // h(-1) = 0, both halves
+        if (threadIdx.x < kF / 8) S.hb[1][threadIdx.x] = make_uint4(0, 0, 0, 0);  // h(-1) = 0, every unit
         cluster_sync_all();
         const int32_t v = S.v;
         if (v < 0) break;
@@ -149,11 +162,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int32_t un = (p0 + kAhead < p1) ? __ldg(col_src + p0 + kAhead) : 0;
         for (int32_t p = p0; p < p1; ++p) {
             const int t = p - p0, bi = (t + 1) & 1, bo = t & 1;  // read h(t-1) from hb[bi], write h(t) to hb[bo]
-            if (t > 0) {  // the peer's half of h(t-1); then re-armed for h(t+1), which the peer
-                          // sends only after it has this CTA's h(t), sent after this point
+            if (t > 0) {  // the other CTAs' units of h(t-1); then re-armed for h(t+1), which they
+                          // send only after they have this CTA's h(t), sent after this point
                 ptx::mbar_wait(&S.hfull[bi], par[bi]);
                 par[bi] ^= 1u;
-                if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(&S.hfull[bi], 64 * 2);
+                if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(&S.hfull[bi], kPeerBytes);
             }
             const float pz = __bfloat162float(ring[0]);
 #pragma unroll
@@ -181,30 +194,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             hf = og * (2.0f * sigm_fast(2.0f * c) - 1.0f);
             if (g == 0) reinterpret_cast<__nv_bfloat16 *>(S.hb[bo])[j] = __float2bfloat16_rn(hf);
             __syncwarp();
-            if (lane == 0) {  // this warp's 8 units of h(t) into the peer's hb[bo]
-                const uint4 x = S.hb[bo][8 * (int)rank + warp];
-                asm volatile(
-                    "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                        bo ? rh1 : rh0),
-                    "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w), "r"(bo ? rb1 : rb0)
-                    : "memory");
+            if (lane == 0) {  // this warp's 8 units of h(t) into the other CTAs' hb[bo]
+                const uint4 x = S.hb[bo][chunk];
+#pragma unroll
+                for (int q = 0; q < CS - 1; ++q)
+                    asm volatile(
+                        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, "
+                        "[%5];" ::"r"(bo ? rh[1][q] : rh[0][q]),
+                        "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w), "r"(bo ? rb[1][q] : rb[0][q])
+                        : "memory");
             }
-            __syncthreads();  // this CTA's half of h(t) is visible; every read of hb[bi] is done
+            __syncthreads();  // this CTA's units of h(t) are visible; every read of hb[bi] is done
         }
         if (g == 0) h_out[(int64_t)v * kF + j] = __float2bfloat16_rn(hf);
-        // the peer's half of the last h arrived (keeps the phases of both barriers in step)
+        // the other CTAs' units of the last h arrived (keeps the barrier phases in step)
         const int tl = p1 - p0 - 1, bl = tl & 1;
         ptx::mbar_wait(&S.hfull[bl], par[bl]);
         par[bl] ^= 1u;
-        if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(&S.hfull[bl], 64 * 2);
+        if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(&S.hfull[bl], kPeerBytes);
         __syncthreads();
     }
-    cluster_sync_all();  // no CTA exits while its peer may still write into it
+    cluster_sync_all();  // no CTA exits while another may still write into it
 }
 
 // ------------------------------------------------------------------------
 // The sequences shorter than kLongDeg in batches on the tensor cores
-// (mma.sync m16n8k16, bf16 -> fp32), concurrently with k_lstm_pair on the
+// (mma.sync m16n8k16, bf16 -> fp32), concurrently with k_lstm_cluster on the
 // long ones.  The recurrent GEMV of a step is computed transposed, G^T =
 // W_hh^T . H^T: the 512 gate rows are the MMA's M (W_hh^T resident in
 // registers as A fragments, 64 per thread) and up to 8 sequences (the CTA's
@@ -216,8 +231,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // Each slot walks its own 8-item chunk of the queue (queue[1]; the long items
 // at its head are skipped) and loads its next item while the current one
 // runs, so the next sequence's first P row is prefetched like any step's.
-constexpr int kLongDeg = 2048;  // sequences of at least this many steps go to k_lstm_pair
-constexpr int kLongCtas = 32;   // CTAs for them (16 pairs, one CTA per SM); the batches take the other SMs
+constexpr int kLongDeg = 2048;  // sequences of at least this many steps go to k_lstm_cluster
+constexpr int kLongCluster = 2;  // CTAs per long sequence (a cluster; h exchanged through DSMEM; 4: slower)
+constexpr int kLongCtas = 32;     // CTAs for them (16 pairs, one CTA per SM); the batches take the other SMs
 constexpr int kSlots = 8;
 constexpr int kHP = kF + 8;          // H row pitch (bf16): the B-fragment loads hit 32 distinct banks
 constexpr int kGP = 4 * kF + 4;      // G row pitch (fp32): conflict-free C stores, 16-B rows
@@ -441,7 +457,7 @@ cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const 
         return launch(k_lstm_mma, grid, kThreads, 0, st, g.n, g.row_ptr, g.col_src, g.deg_order, P, W_hh, b_ih,
                       b_hh, h_out, INT32_MAX);
     }
-    // the long sequences on kLongCtas SMs (k_lstm_pair, the caller's stream)
+    // the long sequences on kLongCtas SMs (k_lstm_cluster, the caller's stream)
     // and the batches on the others (k_lstm_mma, a library stream forked and
     // joined with events, so the pair also captures into a CUDA graph)
     std::lock_guard<std::mutex> lock(g_side_mu);
@@ -449,8 +465,23 @@ cudaError_t launch_lstm_gather(const GraphDev &g, const __nv_bfloat16 *P, const 
     if (!ss.st || !ss.fork || !ss.join) return cudaErrorInitializationError;
     if ((e = cudaEventRecord(ss.fork, st))) return e;
     if ((e = cudaStreamWaitEvent(ss.st, ss.fork, 0))) return e;
-    e = launch(k_lstm_pair, (unsigned)kLongCtas, 256, 0, st, g.n, g.row_ptr, g.col_src, g.deg_order, P, wt, b_ih,
-               b_hh, h_out, queue, kLongDeg);
+    {
+        constexpr int CS = kLongCluster;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)kLongCtas);
+        cfg.blockDim = dim3(512 / CS);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k_lstm_cluster<CS>, g.n, (const int64_t *)g.row_ptr, (const int32_t *)g.col_src,
+                               (const int32_t *)g.deg_order, P, (const uint4 *)wt, b_ih, b_hh, h_out, queue,
+                               (int32_t)kLongDeg);
+    }
     if (e) return e;
     e = launch<false>(k_lstm_mma, (unsigned)std::max(1, sms - kLongCtas), kThreads, 0, ss.st, g.n, g.row_ptr,
                       g.col_src, g.deg_order, P, W_hh, b_ih, b_hh, h_out, kLongDeg);
