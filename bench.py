@@ -230,10 +230,12 @@ def algorithmic(cfg, gs=None):
                                     "flops": 2 * nh * (T * f * f + 6 * f * f), "peak": "fp64_pipe"}
     elif cfg.model == "sage_lstm":
         f, fo = cfg.dims
-        # per edge: gather a 1 KB row of P (4 gates bf16); recurrent GEMV 2 * 4f * f FLOPs
-        # bound by the recurrent GEMV on the CUDA-core FMA pipe (FHFMA.BF16): one step = 4f x f FMAs
+        # per edge: gather a 1 KB row of P (4 gates bf16); recurrent GEMV 2 * 4f * f FLOPs.  Round 2:
+        # the short sequences' GEMVs run on the tensor cores (mma.sync bf16), the long ones' on FHFMA
+        # across CTA pairs, so the bf16 tensor peak is the machine's bound for the contraction; the
+        # kernel's real bound is the hub's chain of dependent steps (DESIGN.md NEXT-2)
         out["lstm_gather"] = {"bytes": e * 4 + (n + 1) * 8 + e * 4 * f * 2 + n * f * 2 + 4 * f * f * 2,
-                              "flops": e * 2 * 4 * f * f, "peak": "fma_pipe"}
+                              "flops": e * 2 * 4 * f * f, "peak": "tensor_bf16"}
         out["lstm_input_gemm"] = {"bytes": n * f * 2 + f * f * 2 + n * f * 2, "flops": 2 * n * f * f,
                                   "peak": "tensor_bf16"}
         out["gemm_bf16_tc"] = {"bytes": n * 2 * (2 * f + fo), "flops": 2 * n * 2 * f * fo, "peak": "tensor_bf16"}
@@ -267,7 +269,6 @@ def algorithmic(cfg, gs=None):
     return out
 
 
-FMA_PIPE_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 FP64_PIPE_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
@@ -287,15 +288,6 @@ def roofline_of(name, spec, avg_s, pk, traffic):
         return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
                     peak_note="derived: 148 SM x 64 fp64 FMA/clk x 2 FLOP x 1.965 GHz (the DMMA tensor path and "
                               "DFMA share it: ncu sm__ops_path_tensor_src_fp64 peak 128 ops/clk/SM)")
-    if spec["peak"] == "fma_pipe":
-        # the full-rate FP32 FMA pipe: 148 SMs x 128 FMA/clk x 2 FLOP x 1.965 GHz = 74.4 TFLOP/s.
-        # (Round 1 held the LSTM gather to the half-rate FHFMA.BF16 instruction it uses, 37.2 --
-        # the kernel's own choice, not the machine's bound.)
-        peak = FMA_PIPE_TFLOPS
-        ach = spec["flops"] / avg_s / 1e12
-        return dict(base, bound="alu", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
-                    peak_note="derived: 148 SM x 128 FP32 FMA/clk x 2 FLOP x 1.965 GHz (full-rate FFMA); the "
-                              "LSTM gather's bound is its critical path, see DESIGN.md")
     # tensor: bf16 measured burst peak (MEASURED_PEAKS.json); TF32 and INT8 measured
     # in this run (cuBLAS 8192^3, measured_tensor_peaks), else the nominal ratios
     peak = pk["bf16_tflops"]
