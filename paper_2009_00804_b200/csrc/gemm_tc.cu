@@ -286,6 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // (per-row stores of only the needed rows were slower still:
                     // from the epilogue warps 1.36-1.78 ms, 4 dedicated store warps
                     // 1.41, TMA scatter4 4.0, vs 1.16-1.25 for the tile stores).
+                    // the previous tile's two TMA stores have finished reading both
+                    // staging buffers before they are overwritten
+                    if (et == 0) ptx::bulk_wait_read<0>();
+                    named_bar(1, 128);
                     uint32_t yp[32], op[32];
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {

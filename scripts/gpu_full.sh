@@ -16,8 +16,10 @@ timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG/launches_C5.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_launch.log 2>&1
 for c in C5 C3 C4 C2 C1 C6 C7 C8; do
+  KRE='k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_gcn_epi|k_split|k_gat_maxel'; NC=9
+  [ $c = C7 ] && KRE='k_lstm|k_stage_whh' && NC=6  # the LSTM pair and its W_hh staging
   timeout 300 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/plain_$c.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_segreduce|k_rowwise|k_gemm|k_lstm|k_slice|heavy|k_gcn_epi|k_split|k_gat_maxel' -s 3 -c 9 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s 3 -c $NC \
       -o gpurun_out/$TAG/full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/$TAG/ncu_full_$c.log 2>&1
 done
 ls gpurun_out/$TAG

@@ -25,7 +25,8 @@ LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)
            ("k_gru_heavy_f64", "gru_heavy_f64")],
     "C5": [("SumBf16Op", "agg_gcn_bf16"), ("k_gcn_epi_rows", "agg_gcn_bf16"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C6": [("SumF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3"), ("k_split_rgcn", "rgcn_apply_tf32x3")],
-    "C7": [("k_lstm_gather", "lstm_gather"), ("k_stage_whh", "lstm_gather"), ("k_gemm_bf16_tc", "gemm_bf16_tc")],
+    "C7": [("k_lstm_cluster", "lstm_gather"), ("k_lstm_mma", "lstm_gather"), ("k_stage_whh", "lstm_gather"),
+           ("k_gemm_bf16_tc", "gemm_bf16_tc")],
     "C8": [("EdgeMlpOp", "agg_edge_mlp_f32"), ("k_gemm_tf32split<256", "ggnn_gru_tf32x3"),
            ("k_gemm_i8x", "ggnn_edge_i8x"), ("k_slice_rows", "ggnn_edge_i8x"), ("k_slice_wt_ggnn", "ggnn_edge_i8x"),
            ("k_split_ggnn", "ggnn_split_weights"), ("k_ggnn_heavy_b", "ggnn_heavy_b_f64"),
