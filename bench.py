@@ -185,7 +185,11 @@ def algorithmic(cfg, gs=None):
     (gated, GGNN)."""
     n, e = cfg.n, cfg.num_edges
     out = {}
-    if cfg.model == "gcn" and cfg.dtype == "bf16":
+    if cfg.model == "gcn" and cfg.dtype == "bf16" and cfg.extra.get("fused"):
+        fi, fo = cfg.dims   # NEXT-1: col_src, row_ptr, dinv, every X row once, W, out
+        out["gcn_fused_tc"] = {"bytes": e * 4 + (n + 1) * 8 + n * 4 + n * fi * 2 + fi * fo * 2 + n * fo * 2,
+                               "flops": 2 * e * fi + 2 * n * fi * fo, "peak": "hbm"}
+    elif cfg.model == "gcn" and cfg.dtype == "bf16":
         fi, fo = cfg.dims
         out["gemm_bf16_tc"] = {"bytes": n * fi * 2 + fi * fo * 2 + n * 4 + n * fo * 2, "flops": 2 * n * fi * fo,
                                "peak": "tensor_bf16"}
@@ -462,7 +466,7 @@ def workload_config(cfg):
             "C6": "R-GCN fp32 (NEXT-3), R-MAT N=2^17 E=2^21, 4 relation types, 128->128",
             "C7": "GraphSAGE-LSTM bf16 (NEXT-2), R-MAT N=2^16 E=2^20 distinct, 128->128",
             "C8": "paper-form GGNN fp32 (NEXT-4: edge MLP on [h_src||h_dst] + ReLU, sum, GRU), R-MAT N=2^17 E=2^21, 128"}
-    w = desc.get(cfg.name, cfg.name) + (" [NEXT-1 fused Gather + concat-GEMM]" if cfg.extra.get("fused") else "")
+    w = desc.get(cfg.name, cfg.name) + (" [NEXT-1 fused Gather + ApplyVertex GEMM, one kernel]" if cfg.extra.get("fused") else "")
     return {"workload": f"{cfg.name}: {w}", "vertices": cfg.n, "edges": cfg.num_edges,
             "model": cfg.model, "global_batch": cfg.n, "parallelism": "replicas"}
 
@@ -651,6 +655,7 @@ STAGES = {
     "ggnn_gru_tf32x3": "S5 ApplyVertex",
     "gru_heavy_f64": "S5 ApplyVertex (heavy rows)",
     "sage_fused_tc": "S3+S4+S5 Scatter/Gather/ApplyVertex (fused)",
+    "gcn_fused_tc": "S3+S4+S5 Scatter/Gather/ApplyVertex (fused)",
 }
 
 
@@ -764,8 +769,9 @@ def main():
     ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly (no CUDA graph)")
-    ap.add_argument("--sage-fused", action="store_true",
-                    help="SAGE (C2): Gather fused with the concat-GEMM in one kernel (NEXT-1)")
+    ap.add_argument("--fused", "--sage-fused", dest="sage_fused", action="store_true",
+                    help="NEXT-1: Gather fused with the ApplyVertex tcgen05 GEMM in one kernel "
+                         "(C2: the concat-GEMM; C5: aggregate-first GCN)")
     ap.add_argument("--ref-edges", type=int, default=2_000_000,
                     help="in-edges per oracle sample (bounded CPU work)")
     ap.add_argument("--ref-seconds", type=float, default=10.0,
@@ -784,8 +790,8 @@ def main():
         args.warmup = 3   # timing rule: >= 3 warm-up steps
     cfg = W.CONFIGS[args.config]
     if args.sage_fused:
-        if cfg.model != "sage":
-            raise SystemExit("--sage-fused applies to the SAGE config (C2)")
+        if cfg.name not in ("C2", "C5"):
+            raise SystemExit("--fused applies to the SAGE config (C2) and the GCN-at-scale config (C5)")
         cfg = W.scaled(cfg, cfg.n, cfg.m, cfg.name)
         cfg.extra["fused"] = True
     if args.impl == "reference":

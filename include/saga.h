@@ -89,9 +89,12 @@ typedef struct {
                               /* GAT must be ELU; GATED ignores it (GRU)                   */
     float leaky_slope;        /* GAT LeakyReLU negative slope in [0, 1] (0.2 in config C3) */
     int32_t aggregator;       /* saga_aggregator, GGNN only (else ignored)                 */
-    int32_t fused;            /* SAGE only: 1 = Gather and the concat-GEMM as ONE kernel    */
-                              /* (in_dim 128, out_dim 64 or 128), 0 =   */
-                              /* the two-kernel path (default; measured faster at C2)       */
+    int32_t fused;            /* SAGE, BF16 GCN: 1 = Gather and the ApplyVertex GEMM as ONE */
+                              /* kernel.       */
+                              /* SAGE: in_dim 128, out_dim 64 or 128.  GCN: in_dim 256,     */
+                              /* out_dim 64, 128 or 256, aggregate first (SAGA order), the  */
+                              /* aggregated row rounded to BF16 before the GEMM.  0 = the   */
+                              /* multi-kernel path (default).  Other kinds ignore it.       */
     int32_t workspace_zeroed; /* 1 = the caller guarantees the workspace's ticket-counter   */
                               /* region is zero: the memory was zero-filled before its     */
                               /* first saga_layer call, and since then only completed      */
@@ -174,7 +177,8 @@ SAGA_API saga_status saga_layer_workspace_bytes(saga_model kind, const saga_grap
  *        out[v] = act( sum_{u->v} deg(u)^-1/2 deg(v)^-1/2 x[u] . W + bias )
  *        features F32 (fused aggregate + SIMT GEMV, in_dim in {16, 32, 64, 128},
  *        1 <= out_dim <= 64) or BF16 (tcgen05 GEMM first, then aggregation;
- *        in_dim in {64,128,192,256}, out_dim in {64,128,256}).
+ *        in_dim in {64,128,192,256}, out_dim in {64,128,256}; opts.fused: one
+ *        kernel, aggregation first, in_dim 256).
  *  SAGE  (Table 1; BASELINE.json C2; A11, A12):
  *        out[v] = act( [x[v] || mean_{u->v} x[u]] . W + bias ), W [2*in][out]
  *        BF16, in_dim in {64, 128}, out_dim in {64, 128, 256}.

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libsaga.so")
-SOURCES = ["graph_build.cu", "aggregate.cu", "gemm_tc.cu", "gemm_tf32split.cu", "gemm_i8x.cu", "gru_f64.cu", "lstm_gather.cu", "sage_fused.cu", "saga_host.cu"]
+SOURCES = ["graph_build.cu", "aggregate.cu", "gemm_tc.cu", "gemm_tf32split.cu", "gemm_i8x.cu", "gru_f64.cu", "lstm_gather.cu", "sage_fused.cu", "gcn_fused.cu", "saga_host.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",

@@ -1,0 +1,398 @@
+// gcn_fused.cu -- SURVEY.md 8(f) NEXT-1 for the GCN layer at scale (config C5):
+// the aggregation fused with its tcgen05 GEMM in SAGA order (aggregate first),
+//   out[v] = act((dinv[v] * sum_{u->v} dinv[u] x[u]) . W + b)      (reading A1)
+// in ONE kernel: no pre-projected Y = X W (2 GiB at C5) is written to HBM and
+// read back, and the layer is one launch instead of three.
+//
+// Paper: "fine-grained pipelining the different stages" between Gather and the
+// ApplyVertex GEMM; Table 1 line 177 fixes the GCN
+// stages (Scatter: source features, ApplyEdge: the normalisation weight,
+// Gather: sum, ApplyVertex: GEMM + ReLU).
+//
+// Persistent, one CTA (16 warps) per SM; 128-row tiles of destinations are
+// dealt dynamically (an atomic tile counter, fetched one tile ahead), because
+// a tile's work varies by 10^2x on a power-law graph:
+//   * W^T (pre-staged once per call as the exact shared-memory image, K-major,
+//     128-byte swizzle, 128 KB at out = 256) arrives once per CTA by one bulk
+//     copy and stays resident;
+//   * the 16 warps split the tile's items (edges + row ends) by merge-path,
+//     gather 512-byte bf16 rows (one 16-byte load per lane, U = 8 rows in
+//     flight per warp) and accumulate dinv[u] * x[u] in fp32; a finished row
+//     is scaled by dinv[v], rounded to bf16 and written straight into the A
+//     operand (64 KB, four 64-column K chunks, swizzled); rows split between
+//     warps leave fp32 partials in shared memory, merged after a barrier in
+//     warp order (deterministic);
+//   * one thread issues the 16 tcgen05.mma (M = 128, N = out, K = 16) into
+//     TMEM and the CTA moves on: the tile's epilogue (TMEM -> bias, act, bf16
+//     -> out) runs at the start of the NEXT tile, after that tile's col_src
+//     loads are in flight, so the MMA's latency is hidden behind them.
+// Supported: in = 256, out in {64, 128, 256}; other shapes use the two-kernel
+// path (gemm_tc.cu + aggregate.cu).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+#include "ptx.cuh"
+
+namespace saga {
+namespace {
+
+constexpr int kWarps = 16;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kRows = 128;           // tile rows = UMMA M
+constexpr int kF = 256;              // input width (8 bf16 per lane)
+constexpr int kU = 8;                // rows in flight per warp
+constexpr int kChunk = kRows * 128;  // one 64-column K chunk of A (16 KB)
+constexpr uint32_t kFull = 0xffffffffu;
+
+template <int FO>
+struct Smem {
+    static constexpr int kA = 0;                                 // A: 4 K chunks
+    static constexpr int kB = kA + 4 * kChunk;                   // W^T image: 4 K chunks of FO rows
+    static constexpr int kBBytes = 4 * FO * 128;
+    static constexpr int kPart = kB + kBBytes;                   // [warp][head, tail][2][lane] float4
+    static constexpr int kRend = kPart + kWarps * 2 * 2 * 32 * 16;  // row_ptr[r0 .. r0 + 128] (int32)
+    static constexpr int kRinv = kRend + (kRows + 1) * 4 + 12;   // dinv[r0 ..]
+    static constexpr int kMisc = kRinv + kRows * 4;              // head_row, tail_row [warp], barriers, tmem, tile
+    static constexpr int kBytes = kMisc + 2 * kWarps * 4 + 64 + 1024;  // + alignment slack
+    static_assert(kBytes <= 232448, "shared memory");
+};
+
+// 16 bytes (8 bf16 of row r, columns 8 lane .. 8 lane + 7) into the A operand:
+// K chunk lane / 8, 16-byte unit (lane % 8) XOR (r % 8).
+__device__ __forceinline__ void put_row(uint8_t *A, int r, int lane, const float (&m)[8]) {
+    uint8_t *p = A + (lane >> 3) * kChunk + r * 128 + (((lane & 7) ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4 *>(p) = make_uint4(ptx::pack_bf16x2(m[0], m[1]), ptx::pack_bf16x2(m[2], m[3]),
+                                               ptx::pack_bf16x2(m[4], m[5]), ptx::pack_bf16x2(m[6], m[7]));
+}
+
+template <int FO>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gcn_fused(int32_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_src,
+                const float *__restrict__ dinv, const __nv_bfloat16 *__restrict__ X,
+                const uint8_t *__restrict__ wt_image, const float *__restrict__ bias, int act,
+                __nv_bfloat16 *__restrict__ out, int32_t *tile_ctr) {
+    using S = Smem<FO>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    griddep_wait();  // the W^T image and the zeroed tile counter come from k_stage_gcn
+    uint8_t *A = sm + S::kA;
+    uint8_t *B = sm + S::kB;
+    float4 *part = reinterpret_cast<float4 *>(sm + S::kPart);
+    int32_t *rend = reinterpret_cast<int32_t *>(sm + S::kRend);
+    float *rinv = reinterpret_cast<float *>(sm + S::kRinv);
+    int32_t *head_row = reinterpret_cast<int32_t *>(sm + S::kMisc);
+    int32_t *tail_row = head_row + kWarps;
+    uint64_t *bar_w = reinterpret_cast<uint64_t *>(tail_row + kWarps);
+    uint64_t *bar_mma = bar_w + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_w + 2);
+    int32_t *tile_slot = reinterpret_cast<int32_t *>(tmem_slot + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t ntiles = (n + kRows - 1) / kRows;
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar_w, 1);
+        ptx::mbar_init(bar_mma, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<FO>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) {  // W^T image: once per CTA
+        ptx::mbar_arrive_expect_tx(bar_w, S::kBBytes);
+        ptx::bulk_g2s(B, wt_image, (uint32_t)S::kBBytes, bar_w);
+    }
+    const char *xl = reinterpret_cast<const char *>(X) + lane * 16;
+    auto load = [&](int32_t u) -> uint4 {
+        return __ldg(reinterpret_cast<const uint4 *>(ptx::mad_wide((uint32_t)u, 2u * kF, xl)));
+    };
+
+    // TMEM -> out for the tile whose MMA was committed last: warp -> TMEM lane
+    // quarter warp % 4, columns (warp / 4) * FO / 4 ...
+    auto epilogue = [&](int32_t r0, int nrows) {
+        constexpr int kCols = FO / 4;  // 64, 32 or 16
+        const int qd = warp & 3, cbk = warp >> 2;
+        const int r = qd * 32 + lane;
+#pragma unroll
+        for (int piece = 0; piece < kCols / 16; ++piece) {
+            const int c0 = cbk * kCols + piece * 16;
+            uint32_t vv[16];
+            ptx::tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + c0, vv);
+            ptx::tmem_ld_wait();
+            if (r < nrows) {
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float a = __uint_as_float(vv[2 * i]) + (bias ? __ldg(bias + c0 + 2 * i) : 0.0f);
+                    float b = __uint_as_float(vv[2 * i + 1]) + (bias ? __ldg(bias + c0 + 2 * i + 1) : 0.0f);
+                    if (act == SAGA_ACT_RELU) {
+                        a = fmaxf(a, 0.0f);
+                        b = fmaxf(b, 0.0f);
+                    }
+                    pk[i] = ptx::pack_bf16x2(a, b);
+                }
+                uint4 *o = reinterpret_cast<uint4 *>(out + (int64_t)(r0 + r) * FO + c0);
+                o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+        }
+    };
+
+    uint32_t it = 0;
+    int32_t prev_r0 = -1;
+    int prev_nrows = 0;
+    for (int32_t tile = blockIdx.x; tile < ntiles; ++it) {
+        const int32_t r0 = tile * kRows;
+        const int nrows = min(kRows, n - r0);
+        int32_t nxt = 0;
+        if (threadIdx.x == 0) nxt = (int32_t)gridDim.x + atomicAdd(tile_ctr, 1);  // used at the tile's end
+        // every warp is past the previous tile's gather and merge: the row tables are free
+        for (int i = threadIdx.x; i <= kRows; i += kThreads) rend[i] = (int32_t)row_ptr[r0 + min(i, nrows)];
+        for (int i = threadIdx.x; i < kRows; i += kThreads) rinv[i] = i < nrows ? __ldg(dinv + r0 + i) : 0.0f;
+        if (threadIdx.x < kWarps) head_row[threadIdx.x] = tail_row[threadIdx.x] = -1;
+        __syncthreads();
+
+        // -------------------------------------------- gather: merge-path --
+        const int32_t E0 = rend[0], E1 = rend[nrows];
+        const int32_t items = (E1 - E0) + nrows;
+        const int32_t T = (items + kWarps - 1) / kWarps;
+        auto coord = [&](int32_t d, int32_t &row, int32_t &edge) {  // row = #rows whose end item < d
+            int32_t lo = 0, hi = nrows;
+            while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if ((rend[mid + 1] - E0) + mid >= d)
+                    hi = mid;
+                else
+                    lo = mid + 1;
+            }
+            row = lo;
+            edge = E0 + d - lo;
+        };
+        int32_t v, p, v1, p1;
+        coord(min(warp * T, items), v, p);
+        coord(min((warp + 1) * T, items), v1, p1);
+        const int32_t v0 = v;
+        // sources (and their dinv) in coalesced 32-edge chunks, two chunks ahead;
+        // batches start at p + multiple of kU and kU | 32, so a batch never
+        // straddles a chunk
+        int32_t cb = p;
+        auto load_cs = [&](int32_t base) -> int32_t { return base + lane < p1 ? __ldg(col_src + base + lane) : 0; };
+        int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32), cs_c = load_cs(cb + 64);
+
+        // the previous tile's MMA has had the table loads and the barrier to
+        // retire: drain its accumulator while this tile's sources arrive.
+        // After the wait A is free for this tile's rows.
+        if (prev_r0 >= 0) {
+            ptx::mbar_wait(bar_mma, (it - 1) & 1);
+            ptx::tc_fence_after();
+            epilogue(prev_r0, prev_nrows);
+            ptx::tc_fence_before();
+        }
+
+        float dw_a = __ldg(dinv + cs_a), dw_b = __ldg(dinv + cs_b);
+        auto slide = [&](int32_t qq) {
+            if (qq - cb >= 32) {
+                cb += 32;
+                cs_a = cs_b;
+                dw_a = dw_b;
+                cs_b = cs_c;
+                dw_b = __ldg(dinv + cs_b);
+                cs_c = load_cs(cb + 64);
+            }
+        };
+        bool head_open = v < nrows && rend[v] < p;
+        const bool head = head_open;
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        int32_t row_end = v < nrows ? rend[v + 1] : E1;
+
+        auto flush = [&]() {
+            if (head_open) {
+                float4 *ps = part + (warp * 2 + 0) * 64 + lane;
+                ps[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                ps[32] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                if (lane == 0) head_row[warp] = v;
+                head_open = false;
+            } else {
+                const float sc = rinv[v];
+                float m[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) m[i] = acc[i] * sc;
+                put_row(A, v, lane, m);
+            }
+            ++v;
+            row_end = v < nrows ? rend[v + 1] : E1;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        };
+        auto addw = [&](const uint4 &x, float w) {
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[2 * i] = fmaf(w, __uint_as_float(xs[i] << 16), acc[2 * i]);
+                acc[2 * i + 1] = fmaf(w, __uint_as_float(xs[i] & 0xffff0000u), acc[2 * i + 1]);
+            }
+        };
+        while (v < v1 && row_end <= p) flush();
+        int32_t q = p;
+        for (; q + kU <= p1; q += kU) {
+            slide(q);
+            const int base = q - cb;
+            uint4 val[kU];
+            float wv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                val[u] = load(__shfl_sync(kFull, cs_a, base + u));
+                wv[u] = __shfl_sync(kFull, dw_a, base + u);
+            }
+            if (row_end > q + kU) {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) addw(val[u], wv[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    addw(val[u], wv[u]);
+                    while (v < v1 && row_end == q + u + 1) flush();
+                }
+            }
+        }
+        for (; q < p1; ++q) {
+            slide(q);
+            const uint4 x = load(__shfl_sync(kFull, cs_a, q - cb));
+            addw(x, __shfl_sync(kFull, dw_a, q - cb));
+            while (v < v1 && row_end == q + 1) flush();
+        }
+        while (v < v1) flush();
+        if (v < nrows && p1 > rend[v]) {  // row v has edges in this range and continues past it
+            const int slot = (head && v == v0) ? 0 : 1;  // 0: the whole range inside a row begun earlier
+            float4 *ps = part + (warp * 2 + slot) * 64 + lane;
+            ps[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            ps[32] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            if (lane == 0) (slot ? tail_row : head_row)[warp] = v;
+        }
+        __syncthreads();
+        // rows split between warps: the warp holding the row's start merges, in warp order
+        {
+            const int32_t r = tail_row[warp];
+            if (r >= 0) {
+                const float4 *pa = part + (warp * 2 + 1) * 64 + lane;
+                const float4 a0 = pa[0], a1 = pa[32];
+                float m[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                for (int w2 = warp + 1; w2 < kWarps && head_row[w2] == r; ++w2) {
+                    const float4 *pb = part + (w2 * 2 + 0) * 64 + lane;
+                    const float4 b0 = pb[0], b1 = pb[32];
+                    m[0] += b0.x; m[1] += b0.y; m[2] += b0.z; m[3] += b0.w;
+                    m[4] += b1.x; m[5] += b1.y; m[6] += b1.z; m[7] += b1.w;
+                }
+                const float sc = rinv[r];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) m[i] *= sc;
+                put_row(A, r, lane, m);
+            }
+        }
+        ptx::fence_proxy_async_smem();  // generic smem writes -> visible to the tensor core
+        if (threadIdx.x == 0) *tile_slot = nxt;
+        __syncthreads();
+
+        // -------------------------------------------------------- MMA --
+        if (threadIdx.x == 0) {
+            if (it == 0) ptx::mbar_wait(bar_w, 0);
+            ptx::tc_fence_after();
+            constexpr uint32_t idesc = ptx::make_idesc(1 /*BF16*/, kRows, FO);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t a_base = ptx::smem_u32(A + c * kChunk), b_base = ptx::smem_u32(B + c * FO * 128);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::umma_f16(tmem, ptx::make_sdesc_sw128(a_base + k * 32), ptx::make_sdesc_sw128(b_base + k * 32),
+                                  idesc, (c | k) != 0);
+            }
+            ptx::umma_commit(bar_mma);
+        }
+        prev_r0 = r0;
+        prev_nrows = nrows;
+        tile = *tile_slot;
+    }
+    if (prev_r0 >= 0) {
+        ptx::mbar_wait(bar_mma, (it - 1) & 1);
+        ptx::tc_fence_after();
+        epilogue(prev_r0, prev_nrows);
+        ptx::tc_fence_before();
+    }
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<FO>(tmem);
+}
+
+// W [256][FO] row-major -> the shared-memory image of W^T: 4 K chunks of FO
+// rows x 128 bytes, 16-byte unit u of row n at ((u ^ (n % 8)) << 4) (128-byte
+// swizzle, K-major); also resets the tile counter the fused kernel deals from.
+template <int FO>
+__global__ void k_stage_gcn(const __nv_bfloat16 *__restrict__ W, uint8_t *img, int32_t *tile_ctr) {
+    griddep_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over 4 * FO * 8 units
+    if (i == 0) *tile_ctr = 0;
+    if (i >= 4 * FO * 8) return;
+    const int u = i % 8, nn = (i / 8) % FO, c = i / (8 * FO);
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int k = c * 64 + u * 8 + 2 * e;
+        w[e] = (uint32_t)__bfloat16_as_ushort(W[(int64_t)k * FO + nn]) |
+               ((uint32_t)__bfloat16_as_ushort(W[(int64_t)(k + 1) * FO + nn]) << 16);
+    }
+    *reinterpret_cast<uint4 *>(img + c * FO * 128 + nn * 128 + ((u ^ (nn & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int FO>
+cudaError_t launch_fo(const GraphDev &g, const __nv_bfloat16 *X, const __nv_bfloat16 *W, const float *bias, int act,
+                      __nv_bfloat16 *out, void *ws, cudaStream_t st) {
+    uint8_t *img = static_cast<uint8_t *>(ws);
+    int32_t *ctr = reinterpret_cast<int32_t *>(img + (size_t)4 * FO * 128);
+    cudaError_t e = launch(k_stage_gcn<FO>, (4 * FO * 8 + 255) / 256, 256, 0, st, W, img, ctr);
+    if (e) return e;
+    using S = Smem<FO>;
+    e = cudaFuncSetAttribute(k_gcn_fused<FO>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+    if (e) return e;
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ntiles = (g.n + kRows - 1) / kRows;
+    const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
+    return launch(k_gcn_fused<FO>, grid, kThreads, S::kBytes, st, g.n, g.row_ptr, g.col_src, g.dinv, X,
+                  static_cast<const uint8_t *>(img), bias, act, out, ctr);
+}
+
+}  // namespace
+
+bool gcn_fused_supported(int32_t in_dim, int32_t out_dim) {
+    return in_dim == kF && (out_dim == 64 || out_dim == 128 || out_dim == 256);
+}
+// [W^T image | tile counter]
+size_t gcn_fused_workspace_bytes(int32_t out_dim) { return (size_t)4 * out_dim * 128 + 16; }
+
+cudaError_t launch_gcn_fused(const GraphDev &g, const __nv_bfloat16 *X, int32_t in_dim, const __nv_bfloat16 *W,
+                             int32_t out_dim, const float *bias, int act, __nv_bfloat16 *out, void *ws,
+                             cudaStream_t st, const char **why) {
+    if (g.n == 0) return cudaSuccess;
+    if (!gcn_fused_supported(in_dim, out_dim)) {
+        *why = "fused GCN needs in_dim 256, out_dim 64, 128 or 256";
+        return cudaErrorInvalidValue;
+    }
+    if (g.e >= (int64_t(1) << 31) - 64) {
+        *why = "fused GCN indexes edges with 32 bits";
+        return cudaErrorInvalidValue;
+    }
+    if (out_dim == 256) return launch_fo<256>(g, X, W, bias, act, out, ws, st);
+    if (out_dim == 128) return launch_fo<128>(g, X, W, bias, act, out, ws, st);
+    return launch_fo<64>(g, X, W, bias, act, out, ws, st);
+}
+
+}  // namespace saga

@@ -235,6 +235,14 @@ cudaError_t launch_gru_heavy_f64(const GraphDev &g, const HeavyWs &w, const floa
 // 2-D bf16 row-major [rows][cols] tensor map, {64 col, box_rows row} box, 128B swizzle (gemm_tc.cu).
 bool make_map_bf16(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int box_rows = 128);
 
+// NEXT-1 (GCN, C5): the aggregation fused with its tcgen05 GEMM in SAGA order
+// (gcn_fused.cu); ws = workspace for the staged W^T image and the tile counter.
+bool gcn_fused_supported(int32_t in_dim, int32_t out_dim);
+size_t gcn_fused_workspace_bytes(int32_t out_dim);
+cudaError_t launch_gcn_fused(const GraphDev &g, const __nv_bfloat16 *X, int32_t in_dim, const __nv_bfloat16 *W,
+                             int32_t out_dim, const float *bias, int act, __nv_bfloat16 *out, void *ws,
+                             cudaStream_t st, const char **why);
+
 // NEXT-1: GraphSAGE-mean aggregation fused with its tcgen05 concat-GEMM
 // (sage_fused.cu); img = workspace for the staged W^T image.
 bool sage_fused_supported(int32_t in_dim, int32_t out_dim);

@@ -194,7 +194,10 @@ Plan plan_for(saga_model kind, const saga::GraphDev &g, const saga_layer_opts &o
     p.counters = align_up(sizeof(int32_t) * (nt + 1));
     p.partials = align_up(sizeof(float) * pf * 2 * (nt + 1));
     switch (kind) {
-        case SAGA_GCN: p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0)); break;  // Y bf16
+        case SAGA_GCN:
+            p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.out_dim, 0));                // Y bf16 (two-kernel path)
+            if (o.fused) p.inter1 = align_up(saga::gcn_fused_workspace_bytes(std::max(o.out_dim, 0)));  // W^T image, tile counter
+            break;
         case SAGA_SAGE:
             p.inter0 = align_up((size_t)2 * n * (size_t)std::max(o.in_dim, 0));                // M bf16 (two-kernel path)
             p.inter1 = align_up(saga::sage_fused_workspace_bytes(std::max(o.out_dim, 0)));     // W^T image (fused)
@@ -249,6 +252,8 @@ saga_status validate(saga_model kind, const saga::GraphDev &d, const saga_tensor
             if (o.in_dim % 64 || o.in_dim > 256 || o.in_dim == 0 ||
                 !(o.out_dim == 64 || o.out_dim == 128 || o.out_dim == 256))
                 return fail(SAGA_EUNSUPPORTED, "bf16 GCN supports in_dim in {64..256 step 64}, out_dim in {64,128,256}");
+            if (o.fused && !saga::gcn_fused_supported(o.in_dim, o.out_dim))
+                return fail(SAGA_EUNSUPPORTED, "fused GCN supports in_dim 256, out_dim 64, 128 or 256");
             return SAGA_OK;
         case SAGA_SAGE:
             if (x->dtype != SAGA_BF16) return fail(SAGA_EDTYPE, "SAGE supports BF16 features");
@@ -498,6 +503,17 @@ saga_status saga_layer(saga_model kind, const saga_graph *g, const saga_tensor *
                                              static_cast<float *>(out->data), aw, st);
                 }
                 if (e) return cuda_fail(e, "gcn_f32_fused");
+                return SAGA_OK;
+            }
+            if (o.fused) {
+                // NEXT-1: SAGA order, the aggregation and the ApplyVertex GEMM in one kernel
+                {
+                    ProfScope ps_("gcn_fused_tc", st);
+                    e = launch_gcn_fused(d, static_cast<const __nv_bfloat16 *>(x->data), o.in_dim,
+                                         static_cast<const __nv_bfloat16 *>(w->W), o.out_dim, w->bias, o.act,
+                                         static_cast<__nv_bfloat16 *>(out->data), i1, st, &why);
+                }
+                if (e) return fail(SAGA_ECUDA, "gcn fused: %s (%s)", cudaGetErrorString(e), why);
                 return SAGA_OK;
             }
             // S2: Y = diag(dinv) . X . W  (tcgen05), then S3-S5 aggregation

@@ -54,7 +54,8 @@ def gpu_step(saga, cfg, g, d, layers=None, outs=None):
     act_relu = saga.SAGA_ACT_RELU
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     if cfg.model == "gcn":
-        lay = layers[0] if layers else saga.Layer("gcn", g, cfg.dims[0], cfg.dims[1], act_relu, dt)
+        lay = layers[0] if layers else saga.Layer("gcn", g, cfg.dims[0], cfg.dims[1], act_relu, dt,
+                                                    fused=cfg.extra.get("fused", False))
         return [lay(d["X"], {"W": d["W"], "bias": d["b"]}, out=o(0))], [lay]
     if cfg.model == "sage":
         f0, f1, f2 = cfg.dims

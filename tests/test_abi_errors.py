@@ -189,3 +189,16 @@ def test_sage_fused_rejects_unsupported_widths(saga):
     with pytest.raises(saga.SagaError) as ei:
         saga.saga_layer(saga.SAGA_SAGE, g, x, {"W": w}, out, opts, ws)
     assert ei.value.status == saga.SAGA_EUNSUPPORTED
+
+
+@pytest.mark.gpu
+def test_gcn_fused_rejects_unsupported_widths(saga):
+    g = _graph(saga, 4, [0, 1, 2, 3], [1, 2, 3, 0])
+    x = torch.randn(4, 128, device="cuda").bfloat16()
+    w = torch.randn(128, 64, device="cuda").bfloat16()
+    out = torch.empty(4, 64, dtype=torch.bfloat16, device="cuda")
+    opts = saga.make_opts(128, 64, saga.SAGA_ACT_RELU, fused=1)
+    ws = torch.empty(saga.saga_layer_workspace_bytes(saga.SAGA_GCN, g, opts), dtype=torch.uint8, device="cuda")
+    with pytest.raises(saga.SagaError) as ei:
+        saga.saga_layer(saga.SAGA_GCN, g, x, {"W": w}, out, opts, ws)
+    assert ei.value.status == saga.SAGA_EUNSUPPORTED

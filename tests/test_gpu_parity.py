@@ -355,6 +355,54 @@ def _random_graph(seed):
     return n, s, d
 
 
+@pytest.mark.parametrize("size", ["full_sampled", "ragged", "tiny"])
+def test_gcn_fused_next1(saga, size):
+    """NEXT-1 for C5: the GCN aggregation fused with its tcgen05 GEMM in SAGA
+    order (one kernel), at C5 full size on sampled rows
+    (hubs included; the launch configuration the bench times), a ragged size
+    (last tile partial, hubs split across warps, dynamic tiles) and a graph
+    smaller than one tile."""
+    c = W.CONFIGS["C5"]
+    if size == "full_sampled":
+        _config_check(saga, _fused(c), rows_k=3000)
+    else:
+        _config_check(saga, {"ragged": _fused(c, 5000, 40000), "tiny": _fused(c, 77, 300)}[size])
+
+
+@pytest.mark.parametrize("fo", [64, 128, 256])
+@pytest.mark.parametrize("name,n,s,d", ZOO, ids=lambda x: x if isinstance(x, str) else "")
+@pytest.mark.parametrize("loops", [False, True])
+def test_gcn_fused_zoo(saga, name, n, s, d, loops, fo):
+    """The zoo (empty rows, stars, the 70K-edge hub, non-multiples of the tile)
+    through the fused GCN at every supported output width."""
+    if fo != 256 and name not in ("hub70k", "multigraph333"):
+        pytest.skip("narrow outputs: two zoo graphs")
+    if loops:
+        s, d = zoo.with_self_loops(n, s, d)
+    _gcn_fused_case(saga, n, s, d, fo, 7, f"fused gcn/{name}/loops={loops}/fo={fo}")
+
+
+def _gcn_fused_case(saga, n, s, d, fo, seed, label):
+    gen = torch.Generator().manual_seed(seed)
+    r = lambda *sh, sc=1.0: torch.randn(*sh, generator=gen) * sc
+    x = {"X": r(n, 256).bfloat16(), "W": r(256, fo, sc=0.1).bfloat16(), "b": r(fo, sc=0.1)}
+    x["src"], x["dst"] = torch.from_numpy(s), torch.from_numpy(d)
+    cfg = W.Config("zg", "gcn", "er", n, s.shape[0], False, False, "bf16", (256, fo), extra={"fused": True})
+    dx = H.dev_inputs(x, DEV)
+    g = H.gpu_graph(saga, cfg, dx)
+    outs, _ = H.gpu_step(saga, cfg, g, dx)
+    torch.cuda.synchronize()
+    og = H.oracle_graph(oracle, cfg, x)
+    ref = H.oracle_step(oracle, cfg, og, x)[0]
+    H.check(outs[0], ref, H.TOL["bf16"], label)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_gcn_fused_random_graphs(saga, seed):
+    n, s, d = _random_graph(1000 * seed + 7)
+    _gcn_fused_case(saga, n, s, d, [256, 128, 64][seed % 3], seed, f"fused gcn/seed {seed} (n={n}, e={s.shape[0]})")
+
+
 @pytest.mark.parametrize("seed", range(40))
 @pytest.mark.parametrize("model", ["gcn_bf16", "gcn_f32", "sage", "sage_fused", "gat", "gated", "rgcn", "ggnn",
                                    "ggnn_max", "sage_lstm"])
