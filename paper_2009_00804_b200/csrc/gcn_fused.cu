@@ -10,14 +10,19 @@
 // Gather: sum, ApplyVertex: GEMM + ReLU).
 //
 // Persistent, one CTA (16 warps) per SM; 128-row tiles of destinations are
-// dealt dynamically (an atomic tile counter, fetched one tile ahead), because
-// a tile's work varies by 10^2x on a power-law graph:
+// dealt dynamically (an atomic tile counter, fetched two tiles ahead), because
+// a tile's work varies by 10^2x on a power-law graph.  The dependent cold
+// loads at a tile's start (row_ptr -> col_src -> rows) are taken off the
+// critical path: the next tile's row tables travel in registers during this
+// tile's gather, and each warp plans its share of the next tile and issues
+// its first col_src chunks before the barrier that precedes this tile's MMA.
 //   * W^T (pre-staged once per call as the exact shared-memory image, K-major,
 //     128-byte swizzle, 128 KB at out = 256) arrives once per CTA by one bulk
 //     copy and stays resident;
 //   * the 16 warps split the tile's items (edges + row ends) by merge-path,
-//     gather 512-byte bf16 rows (one 16-byte load per lane, U = 8 rows in
-//     flight per warp) and accumulate dinv[u] * x[u] in fp32; a finished row
+//     gather 512-byte bf16 rows (one 16-byte load per lane, batches of U = 8
+//     rows, each batch prefetched into L2 two batches ahead of its loads) and
+//     accumulate dinv[u] * x[u] in fp32; a finished row
 //     is scaled by dinv[v], rounded to bf16 and written straight into the A
 //     operand (64 KB, four 64-column K chunks, swizzled); rows split between
 //     warps leave fp32 partials in shared memory, merged after a barrier in
@@ -40,11 +45,12 @@
 namespace saga {
 namespace {
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 32;             // 64 registers per thread
 constexpr int kThreads = 32 * kWarps;
 constexpr int kRows = 128;           // tile rows = UMMA M
 constexpr int kF = 256;              // input width (8 bf16 per lane)
-constexpr int kU = 8;                // rows in flight per warp
+constexpr int kU = 4;                // rows per batch
+constexpr int kAhead = 2;            // batches prefetched into L2 ahead of the loads
 constexpr int kChunk = kRows * 128;  // one 64-column K chunk of A (16 KB)
 constexpr uint32_t kFull = 0xffffffffu;
 
@@ -53,11 +59,12 @@ struct Smem {
     static constexpr int kA = 0;                                 // A: 4 K chunks
     static constexpr int kB = kA + 4 * kChunk;                   // W^T image: 4 K chunks of FO rows
     static constexpr int kBBytes = 4 * FO * 128;
-    static constexpr int kPart = kB + kBBytes;                   // [warp][head, tail][2][lane] float4
-    static constexpr int kRend = kPart + kWarps * 2 * 2 * 32 * 16;  // row_ptr[r0 .. r0 + 128] (int32)
-    static constexpr int kRinv = kRend + (kRows + 1) * 4 + 12;   // dinv[r0 ..]
-    static constexpr int kMisc = kRinv + kRows * 4;              // head_row, tail_row [warp], barriers, tmem, tile
-    static constexpr int kBytes = kMisc + 2 * kWarps * 4 + 64 + 1024;  // + alignment slack
+    static constexpr int kPart = kB + kBBytes;                   // [warp][2][lane] float4: the warp's head partial
+    static constexpr int kRendStride = kRows + 4;                // int32 per table buffer (129 used)
+    static constexpr int kRend = kPart + kWarps * 2 * 32 * 16;  // 2 x row_ptr[r0 .. r0 + 128] (int32)
+    static constexpr int kRinv = kRend + 2 * kRendStride * 4;    // 2 x dinv[r0 ..]
+    static constexpr int kMisc = kRinv + 2 * kRows * 4;          // head_row [warp], barriers, tmem, tile
+    static constexpr int kBytes = kMisc + kWarps * 4 + 64;   // the dynamic window is 1024-byte aligned (checked)
     static_assert(kBytes <= 232448, "shared memory");
 };
 
@@ -76,17 +83,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint8_t *__restrict__ wt_image, const float *__restrict__ bias, int act,
                 __nv_bfloat16 *__restrict__ out, int32_t *tile_ctr) {
     using S = Smem<FO>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t sm[];
+    if ((ptx::smem_u32(sm) & 1023u) != 0) __trap();  // the swizzled operands need 1024-byte alignment
     griddep_wait();  // the W^T image and the zeroed tile counter come from k_stage_gcn
     uint8_t *A = sm + S::kA;
     uint8_t *B = sm + S::kB;
     float4 *part = reinterpret_cast<float4 *>(sm + S::kPart);
-    int32_t *rend = reinterpret_cast<int32_t *>(sm + S::kRend);
-    float *rinv = reinterpret_cast<float *>(sm + S::kRinv);
+    int32_t *rend2 = reinterpret_cast<int32_t *>(sm + S::kRend);
+    float *rinv2 = reinterpret_cast<float *>(sm + S::kRinv);
     int32_t *head_row = reinterpret_cast<int32_t *>(sm + S::kMisc);
-    int32_t *tail_row = head_row + kWarps;
-    uint64_t *bar_w = reinterpret_cast<uint64_t *>(tail_row + kWarps);
+    uint64_t *bar_w = reinterpret_cast<uint64_t *>(head_row + kWarps);
     uint64_t *bar_mma = bar_w + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_w + 2);
     int32_t *tile_slot = reinterpret_cast<int32_t *>(tmem_slot + 1);
@@ -114,9 +120,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     // TMEM -> out for the tile whose MMA was committed last: warp -> TMEM lane
-    // quarter warp % 4, columns (warp / 4) * FO / 4 ...
+    // quarter warp % 4, columns (warp / 4) * FO / (kWarps / 4) ...
     auto epilogue = [&](int32_t r0, int nrows) {
-        constexpr int kCols = FO / 4;  // 64, 32 or 16
+        constexpr int kEpiWarps = 4 * (kWarps / 4 < FO / 16 ? kWarps / 4 : FO / 16);
+        constexpr int kCols = FO / (kEpiWarps / 4);
+        if (warp >= kEpiWarps) return;
         const int qd = warp & 3, cbk = warp >> 2;
         const int r = qd * 32 + lane;
 #pragma unroll
@@ -144,29 +152,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
 
-    uint32_t it = 0;
-    int32_t prev_r0 = -1;
-    int prev_nrows = 0;
-    for (int32_t tile = blockIdx.x; tile < ntiles; ++it) {
-        const int32_t r0 = tile * kRows;
-        const int nrows = min(kRows, n - r0);
-        int32_t nxt = 0;
-        if (threadIdx.x == 0) nxt = (int32_t)gridDim.x + atomicAdd(tile_ctr, 1);  // used at the tile's end
-        // every warp is past the previous tile's gather and merge: the row tables are free
-        for (int i = threadIdx.x; i <= kRows; i += kThreads) rend[i] = (int32_t)row_ptr[r0 + min(i, nrows)];
-        for (int i = threadIdx.x; i < kRows; i += kThreads) rinv[i] = i < nrows ? __ldg(dinv + r0 + i) : 0.0f;
-        if (threadIdx.x < kWarps) head_row[threadIdx.x] = tail_row[threadIdx.x] = -1;
-        __syncthreads();
-
-        // -------------------------------------------- gather: merge-path --
-        const int32_t E0 = rend[0], E1 = rend[nrows];
-        const int32_t items = (E1 - E0) + nrows;
+    // A tile's row tables (row_ptr as int32, dinv): thread t holds entry t in
+    // registers from the global load until the store into a table buffer.
+    auto table_load = [&](int32_t t, int32_t &e_reg, float &d_reg) {
+        const int32_t tr0 = t * kRows;
+        const int tn = min(kRows, n - tr0);
+        const int i = threadIdx.x;
+        if (i <= kRows) e_reg = (int32_t)__ldg(row_ptr + tr0 + min(i, tn));
+        if (i < kRows) d_reg = i < tn ? __ldg(dinv + tr0 + i) : 0.0f;
+    };
+    auto table_store = [&](int buf, int32_t e_reg, float d_reg) {
+        const int i = threadIdx.x;
+        if (i <= kRows) rend2[buf * S::kRendStride + i] = e_reg;
+        if (i < kRows) rinv2[buf * kRows + i] = d_reg;
+    };
+    // A warp's share of a tile's items (edges + row ends, merge-path) and the
+    // first three 32-edge chunks of its sources, loaded coalesced.
+    auto plan = [&](const int32_t *re, int nr, int32_t &v, int32_t &p, int32_t &v1, int32_t &p1, int32_t &ca,
+                    int32_t &cb2, int32_t &cc) {
+        const int32_t E0 = re[0];
+        const int32_t items = (re[nr] - E0) + nr;
         const int32_t T = (items + kWarps - 1) / kWarps;
         auto coord = [&](int32_t d, int32_t &row, int32_t &edge) {  // row = #rows whose end item < d
-            int32_t lo = 0, hi = nrows;
+            int32_t lo = 0, hi = nr;
             while (lo < hi) {
                 const int32_t mid = (lo + hi) >> 1;
-                if ((rend[mid + 1] - E0) + mid >= d)
+                if ((re[mid + 1] - E0) + mid >= d)
                     hi = mid;
                 else
                     lo = mid + 1;
@@ -174,18 +185,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             row = lo;
             edge = E0 + d - lo;
         };
-        int32_t v, p, v1, p1;
         coord(min(warp * T, items), v, p);
         coord(min((warp + 1) * T, items), v1, p1);
-        const int32_t v0 = v;
-        // sources (and their dinv) in coalesced 32-edge chunks, two chunks ahead;
-        // batches start at p + multiple of kU and kU | 32, so a batch never
-        // straddles a chunk
-        int32_t cb = p;
-        auto load_cs = [&](int32_t base) -> int32_t { return base + lane < p1 ? __ldg(col_src + base + lane) : 0; };
-        int32_t cs_a = load_cs(cb), cs_b = load_cs(cb + 32), cs_c = load_cs(cb + 64);
+        ca = p + lane < p1 ? __ldg(col_src + p + lane) : 0;
+        cb2 = p + 32 + lane < p1 ? __ldg(col_src + p + 32 + lane) : 0;
+        cc = p + 64 + lane < p1 ? __ldg(col_src + p + 64 + lane) : 0;
+    };
 
-        // the previous tile's MMA has had the table loads and the barrier to
+    // Tiles: blockIdx.x and blockIdx.x + gridDim.x are this CTA's first two;
+    // the rest are dealt from the counter, fetched two tiles ahead.
+    int32_t tile = blockIdx.x, tile_next = blockIdx.x + gridDim.x;
+    int32_t e_reg = 0;
+    float d_reg = 0.0f;
+    table_load(tile, e_reg, d_reg);
+    table_store(0, e_reg, d_reg);
+    if (lane == 0) head_row[warp] = -1;
+    __syncthreads();
+    int32_t v, p, v1, p1, cs_a, cs_b, cs_c;
+    plan(rend2, min(kRows, n - tile * kRows), v, p, v1, p1, cs_a, cs_b, cs_c);
+    if (tile_next < ntiles) table_load(tile_next, e_reg, d_reg);
+
+    int32_t prev_r0 = -1;
+    int prev_nrows = 0;
+    for (uint32_t it = 0;; ++it) {
+        const int32_t r0 = tile * kRows;
+        const int nrows = min(kRows, n - r0);
+        const int32_t *rend = rend2 + (it & 1) * S::kRendStride;
+        const float *rinv = rinv2 + (it & 1) * kRows;
+        const bool has_next = tile_next < ntiles;
+        int32_t nn = 0;
+        if (threadIdx.x == 0) nn = 2 * (int32_t)gridDim.x + atomicAdd(tile_ctr, 1);  // used at the tile's end
+
+        // the previous tile's MMA has had a barrier and this tile's planning to
         // retire: drain its accumulator while this tile's sources arrive.
         // After the wait A is free for this tile's rows.
         if (prev_r0 >= 0) {
@@ -195,6 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
         }
 
+        // -------------------------------------------- gather: merge-path --
+        // sources (and their dinv) in coalesced 32-edge chunks, two chunks ahead;
+        // batches start at p + multiple of kU and kU | 32, so a batch never
+        // straddles a chunk
+        const int32_t E1 = rend[nrows];
+        const int32_t v0 = v;
+        int32_t cb = p;
+        auto load_cs = [&](int32_t base) -> int32_t { return base + lane < p1 ? __ldg(col_src + base + lane) : 0; };
         float dw_a = __ldg(dinv + cs_a), dw_b = __ldg(dinv + cs_b);
         auto slide = [&](int32_t qq) {
             if (qq - cb >= 32) {
@@ -215,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         auto flush = [&]() {
             if (head_open) {
-                float4 *ps = part + (warp * 2 + 0) * 64 + lane;
+                float4 *ps = part + warp * 64 + lane;
                 ps[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
                 ps[32] = make_float4(acc[4], acc[5], acc[6], acc[7]);
                 if (lane == 0) head_row[warp] = v;
@@ -240,65 +279,93 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc[2 * i + 1] = fmaf(w, __uint_as_float(xs[i] & 0xffff0000u), acc[2 * i + 1]);
             }
         };
-        while (v < v1 && row_end <= p) flush();
-        int32_t q = p;
-        for (; q + kU <= p1; q += kU) {
-            slide(q);
-            const int base = q - cb;
-            uint4 val[kU];
-            float wv[kU];
+        // A batch of kU edges from qq.  Registers hold one batch (two batches
+        // per warp at 16 warps left the compiler moving freshly loaded rows
+        // between registers, which waits for each load where it is issued);
+        // the DRAM latency is taken by an L2 prefetch of the batch kAhead
+        // ahead instead -- one instruction per row, lane i touching bytes
+        // 16 i .. 16 i + 15, no register held -- so the loads that fill the
+        // registers find their rows in L2.  Every load is unconditional:
+        // positions past the range re-read the range's last source with
+        // weight zero (a row the accumulator they reach already holds, or an
+        // accumulator that is never written).
+        auto prefetch = [&](int32_t qq) {  // qq = first edge of the batch to prefetch (a multiple of kU past p)
+            const int idx = qq - cb;        // < 64: the batch lies in chunk a or b (never straddles)
+            const int32_t chunk = idx < 32 ? cs_a : cs_b;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                val[u] = load(__shfl_sync(kFull, cs_a, base + u));
-                wv[u] = __shfl_sync(kFull, dw_a, base + u);
+                const int32_t s = __shfl_sync(kFull, chunk, (idx + u) & 31);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptx::mad_wide((uint32_t)s, 2u * kF, xl)));
             }
-            if (row_end > q + kU) {
+        };
+        while (v < v1 && row_end <= p) flush();
+        if (p < p1) {
 #pragma unroll
-                for (int u = 0; u < kU; ++u) addw(val[u], wv[u]);
-            } else {
+            for (int a = 1; a < kAhead; ++a)
+                if (p + a * kU < p1) prefetch(p + a * kU);
+            for (int32_t q = p; q < p1; q += kU) {
+                slide(q);
+                const int base = q - cb;
+                const int last = p1 - 1 - cb;
+                if (q + kAhead * kU < p1) prefetch(q + kAhead * kU);
+                uint4 val[kU];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    addw(val[u], wv[u]);
-                    while (v < v1 && row_end == q + u + 1) flush();
+                for (int u = 0; u < kU; ++u) val[u] = load(__shfl_sync(kFull, cs_a, min(base + u, last)));
+                if (row_end > q + kU) {
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const float w = __shfl_sync(kFull, dw_a, base + u);
+                        addw(val[u], q + u < p1 ? w : 0.0f);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const float w = __shfl_sync(kFull, dw_a, base + u);
+                        addw(val[u], q + u < p1 ? w : 0.0f);
+                        while (v < v1 && row_end == q + u + 1) flush();
+                    }
                 }
             }
-        }
-        for (; q < p1; ++q) {
-            slide(q);
-            const uint4 x = load(__shfl_sync(kFull, cs_a, q - cb));
-            addw(x, __shfl_sync(kFull, dw_a, q - cb));
-            while (v < v1 && row_end == q + 1) flush();
         }
         while (v < v1) flush();
-        if (v < nrows && p1 > rend[v]) {  // row v has edges in this range and continues past it
-            const int slot = (head && v == v0) ? 0 : 1;  // 0: the whole range inside a row begun earlier
-            float4 *ps = part + (warp * 2 + slot) * 64 + lane;
-            ps[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            ps[32] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            if (lane == 0) (slot ? tail_row : head_row)[warp] = v;
-        }
-        __syncthreads();
-        // rows split between warps: the warp holding the row's start merges, in warp order
-        {
-            const int32_t r = tail_row[warp];
-            if (r >= 0) {
-                const float4 *pa = part + (warp * 2 + 1) * 64 + lane;
-                const float4 a0 = pa[0], a1 = pa[32];
-                float m[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                for (int w2 = warp + 1; w2 < kWarps && head_row[w2] == r; ++w2) {
-                    const float4 *pb = part + (w2 * 2 + 0) * 64 + lane;
-                    const float4 b0 = pb[0], b1 = pb[32];
-                    m[0] += b0.x; m[1] += b0.y; m[2] += b0.z; m[3] += b0.w;
-                    m[4] += b1.x; m[5] += b1.y; m[6] += b1.z; m[7] += b1.w;
-                }
-                const float sc = rinv[r];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) m[i] *= sc;
-                put_row(A, r, lane, m);
+        // row v has edges in this range and continues past it: a range wholly
+        // inside a row begun earlier leaves a head partial; otherwise this
+        // warp holds the row's start and keeps the partial in its registers
+        int32_t tail = -1;
+        if (v < nrows && p1 > rend[v]) {
+            if (head && v == v0) {
+                float4 *ps = part + warp * 64 + lane;
+                ps[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                ps[32] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                if (lane == 0) head_row[warp] = v;
+            } else {
+                tail = v;
             }
         }
+        // the next tile's tables (in registers since the previous tile's end)
+        if (has_next) table_store((it + 1) & 1, e_reg, d_reg);
+        __syncthreads();
+        // rows split between warps: the warp holding the row's start merges, in warp order
+        if (tail >= 0) {
+            for (int w2 = warp + 1; w2 < kWarps && head_row[w2] == tail; ++w2) {
+                const float4 *pb = part + w2 * 64 + lane;
+                const float4 b0 = pb[0], b1 = pb[32];
+                acc[0] += b0.x; acc[1] += b0.y; acc[2] += b0.z; acc[3] += b0.w;
+                acc[4] += b1.x; acc[5] += b1.y; acc[6] += b1.z; acc[7] += b1.w;
+            }
+            const float sc = rinv[tail];
+            float m[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = acc[i] * sc;
+            put_row(A, tail, lane, m);
+        }
         ptx::fence_proxy_async_smem();  // generic smem writes -> visible to the tensor core
-        if (threadIdx.x == 0) *tile_slot = nxt;
+        // the next tile's share and its first source chunks: in flight across
+        // the barrier, the MMA issue and the epilogue
+        if (has_next)
+            plan(rend2 + ((it + 1) & 1) * S::kRendStride, min(kRows, n - tile_next * kRows), v, p, v1, p1, cs_a, cs_b,
+                 cs_c);
+        if (threadIdx.x == 0) *tile_slot = nn;
         __syncthreads();
 
         // -------------------------------------------------------- MMA --
@@ -318,13 +385,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         prev_r0 = r0;
         prev_nrows = nrows;
-        tile = *tile_slot;
-    }
-    if (prev_r0 >= 0) {
-        ptx::mbar_wait(bar_mma, (it - 1) & 1);
-        ptx::tc_fence_after();
-        epilogue(prev_r0, prev_nrows);
-        ptx::tc_fence_before();
+        if (lane == 0) head_row[warp] = -1;  // every merge is past the barrier
+        if (!has_next) {
+            ptx::mbar_wait(bar_mma, it & 1);
+            ptx::tc_fence_after();
+            epilogue(prev_r0, prev_nrows);
+            ptx::tc_fence_before();
+            break;
+        }
+        tile = tile_next;
+        tile_next = *tile_slot;
+        if (tile_next < ntiles) table_load(tile_next, e_reg, d_reg);
     }
     __syncthreads();
     ptx::tc_fence_after();
