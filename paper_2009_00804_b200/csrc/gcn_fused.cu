@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -289,13 +290,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         // positions past the range re-read the range's last source with
         // weight zero (a row the accumulator they reach already holds, or an
         // accumulator that is never written).
+        const char *xh = reinterpret_cast<const char *>(X) + (lane & 15) * 32;
         auto prefetch = [&](int32_t qq) {  // qq = first edge of the batch to prefetch (a multiple of kU past p)
-            const int idx = qq - cb;        // < 64: the batch lies in chunk a or b (never straddles)
-            const int32_t chunk = idx < 32 ? cs_a : cs_b;
+            const int idx = qq - cb + (lane >> 4);  // < 64: the batch lies in chunk a or b (never straddles)
+            const int32_t chunk = qq - cb < 32 ? cs_a : cs_b;
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
+            for (int u = 0; u < kU; u += 2) {  // one instruction per two rows: a half-warp covers a row's 16 sectors
                 const int32_t s = __shfl_sync(kFull, chunk, (idx + u) & 31);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptx::mad_wide((uint32_t)s, 2u * kF, xl)));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptx::mad_wide((uint32_t)s, 2u * kF, xh)));
+            }
+        };
+        // kPad: the range's last, partial batch (positions past p1 clamped)
+        auto batch = [&](int32_t q, auto pad) {
+            constexpr bool kPad = decltype(pad)::value;
+            slide(q);
+            const int base = q - cb;
+            const int last = p1 - 1 - cb;
+            if (q + kAhead * kU < p1) prefetch(q + kAhead * kU);
+            uint4 val[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                val[u] = load(__shfl_sync(kFull, cs_a, kPad ? min(base + u, last) : base + u));
+            auto weight = [&](int u) -> float {
+                const float w = __shfl_sync(kFull, dw_a, base + u);
+                return kPad ? (q + u < p1 ? w : 0.0f) : w;
+            };
+            if (row_end > q + kU) {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) addw(val[u], weight(u));
+            } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    addw(val[u], weight(u));
+                    while (v < v1 && row_end == q + u + 1) flush();
+                }
             }
         };
         while (v < v1 && row_end <= p) flush();
@@ -303,29 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int a = 1; a < kAhead; ++a)
                 if (p + a * kU < p1) prefetch(p + a * kU);
-            for (int32_t q = p; q < p1; q += kU) {
-                slide(q);
-                const int base = q - cb;
-                const int last = p1 - 1 - cb;
-                if (q + kAhead * kU < p1) prefetch(q + kAhead * kU);
-                uint4 val[kU];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) val[u] = load(__shfl_sync(kFull, cs_a, min(base + u, last)));
-                if (row_end > q + kU) {
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        const float w = __shfl_sync(kFull, dw_a, base + u);
-                        addw(val[u], q + u < p1 ? w : 0.0f);
-                    }
-                } else {
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        const float w = __shfl_sync(kFull, dw_a, base + u);
-                        addw(val[u], q + u < p1 ? w : 0.0f);
-                        while (v < v1 && row_end == q + u + 1) flush();
-                    }
-                }
-            }
+            int32_t q = p;
+            for (; q + kU <= p1; q += kU) batch(q, std::false_type{});
+            if (q < p1) batch(q, std::true_type{});
         }
         while (v < v1) flush();
         // row v has edges in this range and continues past it: a range wholly
