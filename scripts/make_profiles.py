@@ -27,6 +27,7 @@ LABELS = {  # config -> [(substring of the ncu kernel name, bench/profile label)
     "C6": [("SumF32Op", "agg_typed_mean_f32"), ("k_gemm_tf32split", "rgcn_apply_tf32x3"), ("k_split_rgcn", "rgcn_apply_tf32x3")],
     "C7": [("k_lstm_cluster", "lstm_gather"), ("k_lstm_mma", "lstm_gather"), ("k_stage_whh", "lstm_gather"),
            ("k_gemm_bf16_tc", "gemm_bf16_tc")],
+    "C5_fused": [("k_gcn_fused", "gcn_fused_tc")],
     "C8": [("EdgeMlpOp", "agg_edge_mlp_f32"), ("k_gemm_tf32split<256", "ggnn_gru_tf32x3"),
            ("k_gemm_i8x", "ggnn_edge_i8x"), ("k_slice_rows", "ggnn_edge_i8x"), ("k_slice_wt_ggnn", "ggnn_edge_i8x"),
            ("k_split_ggnn", "ggnn_split_weights"), ("k_ggnn_heavy_b", "ggnn_heavy_b_f64"),
@@ -82,6 +83,24 @@ def read_rep(path):
     return rows
 
 
+def stall_lines(rep, out_path, top=30):
+    """The SASS instructions holding the most warp-stall samples (ncu source page)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr = next((i for i, r in enumerate(rows) if r and r[0] == "Address"), None)
+    if hdr is None:
+        return
+    body = [r for r in rows[hdr + 1:] if len(r) > 5]
+    tot = sum(int(r[2]) for r in body) or 1
+    idx = sorted(range(len(body)), key=lambda i: -int(body[i][2]))[:top]
+    lines = [f"# {os.path.basename(rep)}: SASS lines by warp-stall samples (all samples {tot}); index, instruction, "
+             "samples, share, warp-level executions"]
+    for i in sorted(idx):
+        r = body[i]
+        lines.append(f"{i:5d}  {r[1].strip()[:90]:90s} {r[2]:>8s} {100 * int(r[2]) / tot:5.1f}%  exec {r[5]}")
+    open(out_path, "w").write("\n".join(lines) + "\n")
+
+
 def main(tag, commit="unknown"):
     src = os.path.join(ROOT, "gpurun_out", tag)
     dst = os.path.join(ROOT, "profiles")
@@ -89,7 +108,7 @@ def main(tag, commit="unknown"):
     traffic_path = os.path.join(dst, "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     md = [f"# ncu summary `{tag}` (ncu --set full --clock-control none; cold-cache replays)\n"]
-    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"]:
+    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8", "C5_fused"]:
         rep = os.path.join(src, f"full_{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -107,7 +126,14 @@ def main(tag, commit="unknown"):
             if lab:
                 per[lab][d["name"].split("(")[0]].append(d.get("dram_read", 0) + d.get("dram_write", 0))
         # a label's traffic per call: the mean of each of its kernels, summed over its kernels
-        traffic[cfg] = {lab: sum(sum(v) / len(v) for v in ks.values()) for lab, ks in per.items()}
+        t = {lab: sum(sum(v) / len(v) for v in ks.values()) for lab, ks in per.items()}
+        base = cfg.split("_")[0]  # "C5_fused" (the opt-in NEXT-1 kernel) files under C5
+        if base == cfg:
+            traffic[cfg] = t
+        else:
+            traffic.setdefault(base, {}).update(t)
+        if cfg == "C5_fused":
+            stall_lines(rep, os.path.join(dst, f"{tag}_gcn_fused_stalls.txt"))
     traffic["_commit"] = commit
     traffic["_when"] = tag
     open(os.path.join(dst, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
@@ -134,7 +160,7 @@ def main(tag, commit="unknown"):
         for k, (n, t) in sorted(ours.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"{k},{n},{t:.4f},{t / tot:.4f}")
         open(os.path.join(dst, f"{tag}_launch_shares_C5.csv"), "w").write("\n".join(lines) + "\n")
-    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8"]:
+    for cfg in ["C1", "C2", "C3", "C4", "C5", "C6", "C7", "C8", "C5_fused", "C2_fused"]:
         b = os.path.join(src, f"bench_{cfg}.json")
         if os.path.exists(b):
             shutil.copy(b, os.path.join(dst, f"{tag}_bench_{cfg}.json"))
