@@ -435,12 +435,19 @@ def test_random_graphs(saga, model, seed):
         H.check(y, ref, tol, f"{model}/seed {seed} (n={n}, e={s.shape[0]})/layer{i}")
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C6", "C7", "C8"])
+def _named(cfg):
+    """A BASELINE config by name; "C5f" / "C2f": the same through the NEXT-1 fused kernels."""
+    if cfg.endswith("f"):
+        return _fused(W.CONFIGS[cfg[:-1]])
+    return W.CONFIGS[cfg]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5f", "C6", "C7", "C8"])
 def test_cuda_graph_replay_matches_eager(saga, cfg):
     """bench.py times the step captured in a CUDA graph: the replayed step is
     bit-identical to the eagerly launched one (same kernels, deterministic;
     C7 also forks its batches onto the library stream inside the capture)."""
-    c = W.CONFIGS[cfg]
+    c = _named(cfg)
     if c.n > 200000:
         c = W.scaled(c, 20000, 200000, cfg + "g")
     d = W.make_inputs(c, DEV)
@@ -459,13 +466,13 @@ def test_cuda_graph_replay_matches_eager(saga, cfg):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6", "C7", "C8"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C5f", "C6", "C7", "C8"])
 def test_programmatic_launch_matches_serialised(saga, cfg):
     """Inside a layer call every kernel after the first is a programmatic
     dependent launch (internal.cuh); with per-kernel profiling on, the library
     launches them fully serialised.  Both give bit-identical outputs (each
     kernel waits for its predecessor before reading its output)."""
-    c = W.CONFIGS[cfg]
+    c = _named(cfg)
     if c.n > 200000:
         c = W.scaled(c, 30000, 400000, cfg + "p")
     d = W.make_inputs(c, DEV)
@@ -490,12 +497,12 @@ def test_programmatic_launch_matches_serialised(saga, cfg):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C6", "C7", "C8"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C5f", "C6", "C7", "C8"])
 def test_workspace_zeroed_contract(saga, cfg):
     """opts.workspace_zeroed (include/saga.h): with 0 the library zeroes the
     ticket counters itself (a garbage-filled workspace gives the same output);
     every completed call leaves them zero, so the next call may pass 1."""
-    c = W.CONFIGS[cfg]
+    c = _named(cfg)
     if c.n > 200000:
         c = W.scaled(c, 30000, 400000, cfg + "w")
     d = W.make_inputs(c, DEV)
