@@ -43,6 +43,10 @@
 #include "internal.cuh"
 #include "ptx.cuh"
 
+#ifndef GF_PROBE
+#define GF_PROBE 0  // development timing probes (1: no MMA / epilogue, 2: no row loads); 0 in every build
+#endif
+
 namespace saga {
 namespace {
 
@@ -75,6 +79,15 @@ __device__ __forceinline__ void put_row(uint8_t *A, int r, int lane, const float
     uint8_t *p = A + (lane >> 3) * kChunk + r * 128 + (((lane & 7) ^ (r & 7)) << 4);
     *reinterpret_cast<uint4 *>(p) = make_uint4(ptx::pack_bf16x2(m[0], m[1]), ptx::pack_bf16x2(m[2], m[3]),
                                                ptx::pack_bf16x2(m[4], m[5]), ptx::pack_bf16x2(m[6], m[7]));
+}
+
+// lo += w.lo * x.lo, hi += w.hi * x.hi: bf16 x bf16 products accumulated in
+// fp32 (sm_100 mixed-precision FMA, one FHFMA.BF16 each, no unpacking).
+__device__ __forceinline__ void fma_pair(float &lo, float &hi, uint32_t w, uint32_t x) {
+    asm("{\n.reg .b16 wl, wh, xl, xh;\nmov.b32 {wl, wh}, %2;\nmov.b32 {xl, xh}, %3;\n"
+        "fma.rn.f32.bf16 %0, wl, xl, %0;\nfma.rn.f32.bf16 %1, wh, xh, %1;\n}"
+        : "+f"(lo), "+f"(hi)
+        : "r"(w), "r"(x));
 }
 
 template <int FO>
@@ -123,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMEM -> out for the tile whose MMA was committed last: warp -> TMEM lane
     // quarter warp % 4, columns (warp / 4) * FO / (kWarps / 4) ...
     auto epilogue = [&](int32_t r0, int nrows) {
-        constexpr int kEpiWarps = 4 * (kWarps / 4 < FO / 16 ? kWarps / 4 : FO / 16);
+        constexpr int kWq = kWarps / 4 >= 8 ? 8 : (kWarps / 4 >= 4 ? 4 : 2);  // column groups: a power of two
+        constexpr int kEpiWarps = 4 * (kWq < FO / 16 ? kWq : FO / 16);
         constexpr int kCols = FO / (kEpiWarps / 4);
         if (warp >= kEpiWarps) return;
         const int qd = warp & 3, cbk = warp >> 2;
@@ -217,15 +231,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t nn = 0;
         if (threadIdx.x == 0) nn = 2 * (int32_t)gridDim.x + atomicAdd(tile_ctr, 1);  // used at the tile's end
 
-        // the previous tile's MMA has had a barrier and this tile's planning to
-        // retire: drain its accumulator while this tile's sources arrive.
-        // After the wait A is free for this tile's rows.
-        if (prev_r0 >= 0) {
-            ptx::mbar_wait(bar_mma, (it - 1) & 1);
-            ptx::tc_fence_after();
-            epilogue(prev_r0, prev_nrows);
-            ptx::tc_fence_before();
-        }
+        // The previous tile's MMA still reads A and its accumulator still sits
+        // in TMEM.  Neither is waited for here: the wait moves to this tile's
+        // first write into A (a_free), and the accumulator is drained after
+        // this tile's gather, when the MMA has long retired (probe: waiting
+        // and draining at the tile's top cost 1.5 of 7.25 ms).
+        bool a_free = prev_r0 < 0 || GF_PROBE == 1;
+        auto wait_a = [&]() {
+            if (!a_free) {
+                ptx::mbar_wait(bar_mma, (it - 1) & 1);
+                ptx::tc_fence_after();
+                a_free = true;
+            }
+        };
 
         // -------------------------------------------- gather: merge-path --
         // sources (and their dinv) in coalesced 32-edge chunks, two chunks ahead;
@@ -235,14 +253,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t v0 = v;
         int32_t cb = p;
         auto load_cs = [&](int32_t base) -> int32_t { return base + lane < p1 ? __ldg(col_src + base + lane) : 0; };
-        float dw_a = __ldg(dinv + cs_a), dw_b = __ldg(dinv + cs_b);
+        // a source's weight dinv[u] as a bf16 pair {w, w}: the products run on the
+        // mixed-precision FMA (bf16 x bf16 in fp32, no unpacking).  Rounding
+        // the weight to bf16 is the aggregate-first counterpart of the default
+        // path's bf16 rounding of Y[u] = dinv[u] (x[u] . W) (reading A17).
+        auto wpair = [&](int32_t cs) -> uint32_t {
+            const float w = __ldg(dinv + cs);
+            return ptx::pack_bf16x2(w, w);
+        };
+        uint32_t dw_a = wpair(cs_a), dw_b = wpair(cs_b);
         auto slide = [&](int32_t qq) {
             if (qq - cb >= 32) {
                 cb += 32;
                 cs_a = cs_b;
                 dw_a = dw_b;
                 cs_b = cs_c;
-                dw_b = __ldg(dinv + cs_b);
+                dw_b = wpair(cs_b);
                 cs_c = load_cs(cb + 64);
             }
         };
@@ -265,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float m[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) m[i] = acc[i] * sc;
+                wait_a();
                 put_row(A, v, lane, m);
             }
             ++v;
@@ -272,13 +299,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0.f;
         };
-        auto addw = [&](const uint4 &x, float w) {
-            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[2 * i] = fmaf(w, __uint_as_float(xs[i] << 16), acc[2 * i]);
-                acc[2 * i + 1] = fmaf(w, __uint_as_float(xs[i] & 0xffff0000u), acc[2 * i + 1]);
-            }
+        auto addw = [&](const uint4 &x, uint32_t w) {
+            fma_pair(acc[0], acc[1], w, x.x);
+            fma_pair(acc[2], acc[3], w, x.y);
+            fma_pair(acc[4], acc[5], w, x.z);
+            fma_pair(acc[6], acc[7], w, x.w);
         };
         // A batch of kU edges from qq.  Registers hold one batch (two batches
         // per warp at 16 warps left the compiler moving freshly loaded rows
@@ -306,14 +331,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             slide(q);
             const int base = q - cb;
             const int last = p1 - 1 - cb;
-            if (q + kAhead * kU < p1) prefetch(q + kAhead * kU);
+            if constexpr (kAhead > 0)
+                if (q + kAhead * kU < p1) prefetch(q + kAhead * kU);
             uint4 val[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u)
+#if GF_PROBE == 2  // timing probe (wrong results): everything but the row loads
+                val[u] = make_uint4(__shfl_sync(kFull, cs_a, base + u), 0u, 0u, 0u);
+#else
                 val[u] = load(__shfl_sync(kFull, cs_a, kPad ? min(base + u, last) : base + u));
-            auto weight = [&](int u) -> float {
-                const float w = __shfl_sync(kFull, dw_a, base + u);
-                return kPad ? (q + u < p1 ? w : 0.0f) : w;
+#endif
+            auto weight = [&](int u) -> uint32_t {
+                const uint32_t w = __shfl_sync(kFull, dw_a, base + u);
+                return kPad ? (q + u < p1 ? w : 0u) : w;
             };
             if (row_end > q + kU) {
 #pragma unroll
@@ -336,6 +366,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (q < p1) batch(q, std::true_type{});
         }
         while (v < v1) flush();
+        // drain the previous tile's accumulator (TMEM -> out); this tile's MMA
+        // is issued only after every warp has passed the two barriers below
+        if (prev_r0 >= 0 && GF_PROBE != 1) {
+            wait_a();
+            epilogue(prev_r0, prev_nrows);
+            ptx::tc_fence_before();
+        }
         // row v has edges in this range and continues past it: a range wholly
         // inside a row begun earlier leaves a head partial; otherwise this
         // warp holds the row's start and keeps the partial in its registers
@@ -377,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
 
         // -------------------------------------------------------- MMA --
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && GF_PROBE != 1) {  // (GF_PROBE 1, timing probe: no MMA, no epilogue)
             if (it == 0) ptx::mbar_wait(bar_w, 0);
             ptx::tc_fence_after();
             constexpr uint32_t idesc = ptx::make_idesc(1 /*BF16*/, kRows, FO);
@@ -395,10 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         prev_nrows = nrows;
         if (lane == 0) head_row[warp] = -1;  // every merge is past the barrier
         if (!has_next) {
-            ptx::mbar_wait(bar_mma, it & 1);
-            ptx::tc_fence_after();
-            epilogue(prev_r0, prev_nrows);
-            ptx::tc_fence_before();
+            if (GF_PROBE != 1) {
+                ptx::mbar_wait(bar_mma, it & 1);
+                ptx::tc_fence_after();
+                epilogue(prev_r0, prev_nrows);
+                ptx::tc_fence_before();
+            } else if (threadIdx.x == 0) {
+                ptx::mbar_wait(bar_w, 0);  // the weight image's bulk copy must land before the CTA exits
+            }
             break;
         }
         tile = tile_next;
