@@ -92,9 +92,10 @@ typedef struct {
     int32_t fused;            /* SAGE, BF16 GCN: 1 = Gather and the ApplyVertex GEMM as ONE */
                               /* kernel.       */
                               /* SAGE: in_dim 128, out_dim 64 or 128.  GCN: in_dim 256,     */
-                              /* out_dim 64, 128 or 256, aggregate first (SAGA order), the  */
-                              /* aggregated row rounded to BF16 before the GEMM.  0 = the   */
-                              /* multi-kernel path (default).  Other kinds ignore it.       */
+                              /* out_dim 64, 128 or 256, E < 2^31 - 64, aggregate first     */
+                              /* (SAGA order): deg(u)^-1/2 and the aggregated row are       */
+                              /* rounded to BF16 (the default rounds Y = XW instead).  0 =  */
+                              /* the multi-kernel path (default).  Other kinds ignore it.   */
     int32_t workspace_zeroed; /* 1 = the caller guarantees the workspace's ticket-counter   */
                               /* region is zero: the memory was zero-filled before its     */
                               /* first saga_layer call, and since then only completed      */
