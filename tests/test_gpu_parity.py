@@ -397,6 +397,14 @@ def _gcn_fused_case(saga, n, s, d, fo, seed, label):
     H.check(outs[0], ref, H.TOL["bf16"], label)
 
 
+def test_gcn_fused_no_edges(saga):
+    """Vertices without any in-edge (dinv = 0): every output row is act(bias);
+    three tiles, the last one partial, no source chunk is ever loaded."""
+    n = 300
+    e = np.zeros(0, dtype=np.int32)
+    _gcn_fused_case(saga, n, e, e, 256, 3, "fused gcn/no edges")
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_gcn_fused_random_graphs(saga, seed):
     n, s, d = _random_graph(1000 * seed + 7)
