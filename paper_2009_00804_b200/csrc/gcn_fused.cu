@@ -9,28 +9,33 @@
 // stages (Scatter: source features, ApplyEdge: the normalisation weight,
 // Gather: sum, ApplyVertex: GEMM + ReLU).
 //
-// Persistent, one CTA (16 warps) per SM; 128-row tiles of destinations are
-// dealt dynamically (an atomic tile counter, fetched two tiles ahead), because
-// a tile's work varies by 10^2x on a power-law graph.  The dependent cold
-// loads at a tile's start (row_ptr -> col_src -> rows) are taken off the
-// critical path: the next tile's row tables travel in registers during this
-// tile's gather, and each warp plans its share of the next tile and issues
-// its first col_src chunks before the barrier that precedes this tile's MMA.
+// Persistent, one CTA (32 warps, 64 registers per thread) per SM; 128-row
+// tiles of destinations are dealt dynamically (an atomic tile counter, fetched
+// two tiles ahead), because a tile's work varies by 10^2x on a power-law
+// graph.  The dependent cold loads at a tile's start (row_ptr -> col_src ->
+// rows) are taken off the critical path: the next tile's row tables travel in
+// registers during this tile's gather, and each warp plans its share of the
+// next tile and issues its first col_src chunks before the barrier that
+// precedes this tile's MMA.
 //   * W^T (pre-staged once per call as the exact shared-memory image, K-major,
 //     128-byte swizzle, 128 KB at out = 256) arrives once per CTA by one bulk
 //     copy and stays resident;
-//   * the 16 warps split the tile's items (edges + row ends) by merge-path,
-//     gather 512-byte bf16 rows (one 16-byte load per lane, batches of U = 8
+//   * the 32 warps split the tile's items (edges + row ends) by merge-path,
+//     gather 512-byte bf16 rows (one 16-byte load per lane, batches of U = 4
 //     rows, each batch prefetched into L2 two batches ahead of its loads) and
-//     accumulate dinv[u] * x[u] in fp32; a finished row
-//     is scaled by dinv[v], rounded to bf16 and written straight into the A
-//     operand (64 KB, four 64-column K chunks, swizzled); rows split between
-//     warps leave fp32 partials in shared memory, merged after a barrier in
-//     warp order (deterministic);
+//     accumulate dinv[u] * x[u] in fp32 on the mixed-precision FMA (dinv[u]
+//     as a bf16 pair); a finished row is scaled by dinv[v], rounded to bf16
+//     and written straight into the A operand (64 KB, four 64-column K
+//     chunks, swizzled); a row split between warps is merged after a barrier
+//     in warp order (deterministic): the warp holding the row's start keeps
+//     its part in registers, the others leave theirs in shared memory;
 //   * one thread issues the 16 tcgen05.mma (M = 128, N = out, K = 16) into
-//     TMEM and the CTA moves on: the tile's epilogue (TMEM -> bias, act, bf16
-//     -> out) runs at the start of the NEXT tile, after that tile's col_src
-//     loads are in flight, so the MMA's latency is hidden behind them.
+//     TMEM and the CTA moves on: the next tile's gather waits for the MMA only
+//     at its first write into A, and the accumulator is drained (TMEM -> bias,
+//     act, bf16 -> out) after that gather, before the next MMA is issued.
+// Measured (C5): 7.23 ms against 3.63 ms for the two-kernel path -- the kernel
+// is bound by its instruction count ("NEXT-1 for C5"), so
+// it is opt-in (opts.fused).
 // Supported: in = 256, out in {64, 128, 256}; other shapes use the two-kernel
 // path (gemm_tc.cu + aggregate.cu).
 #include <cuda.h>
@@ -50,7 +55,7 @@
 namespace saga {
 namespace {
 
-constexpr int kWarps = 32;             // 64 registers per thread
+constexpr int kWarps = 32;            // 64 registers per thread
 constexpr int kThreads = 32 * kWarps;
 constexpr int kRows = 128;           // tile rows = UMMA M
 constexpr int kF = 256;              // input width (8 bf16 per lane)
