@@ -150,3 +150,16 @@ def test_stage_breakdown_and_timeline(bench, tmp_path):
     bench.write_timeline(str(p), c, trace)
     ev = json.load(open(p))["traceEvents"]
     assert len(ev) == 4 and ev[1]["ts"] == pytest.approx(700.0) and ev[1]["dur"] == pytest.approx(3500.0)
+
+
+def test_fused_gcn_model(bench):
+    """--fused on C5 (NEXT-1, gcn_fused.cu): one kernel whose compulsory bytes are
+    col_src, row_ptr, dinv, every X row once, W and the output."""
+    c = W.scaled(W.CONFIGS["C5"], W.CONFIGS["C5"].n, W.CONFIGS["C5"].m, "C5")
+    c.extra["fused"] = True
+    alg = bench.algorithmic(c)
+    assert set(alg) == {"gcn_fused_tc"}
+    n, e = c.n, c.num_edges
+    assert alg["gcn_fused_tc"]["bytes"] == e * 4 + (n + 1) * 8 + n * 4 + n * 256 * 2 + 256 * 256 * 2 + n * 256 * 2
+    assert alg["gcn_fused_tc"]["flops"] == 2 * e * 256 + 2 * n * 256 * 256
+    assert bench.stage_of(c, "gcn_fused_tc").startswith("S3+S4+S5")
